@@ -1,0 +1,124 @@
+"""Oracle: the two skew-Hermitian systems and their shifted resolvents via the
+paper's elliptic reformulations (§2.1 "Reformulation as an elliptic
+problem").
+
+TEST INFRASTRUCTURE ONLY (see oracle/rational.py header).
+
+Resolvent convention (reading R9):
+    (tau L - alpha)^{-1} u0 = (1/tau) (L - beta)^{-1} u0,   beta = alpha / tau.
+
+Example 1, rotating shallow water (Eq. "RSW equations") with
+g = H = 1:   L(v, eta) = (-f J v + grad eta, div v),  J = [[0, 1], [-1, 0]].
+(L - beta)(v, eta) = (v0, eta0) is solved by (derived here; reading R10):
+    v   = A_beta (grad eta - v0),   A_beta = (beta I - f J) / (beta^2 + f^2)
+    (Lap - (beta^2 + f^2)) eta = ((beta^2 + f^2)/beta) (eta0 + div(A_beta v0))
+The paper prints A_alpha = (alpha I + f J)/(alpha^2+f^2); with
+its own L the sign of f must be the one above - the Fourier-mode pin in
+tests/test_oracle_models.py fails for the printed sign.
+
+Example 2, wave equation u_tt = kappa Lap u, state
+(w, z, v) = (u_x, u_y, u_t):  L(w, z, v) = (v_x, v_y, kappa (w_x + z_y)).
+(L - beta)(w, z, v) = (w0, z0, v0) is solved by (Eqs. "w and z eqns",
+"v for inhomog, inverse"):
+    (Lap - beta^2/kappa) v = (beta/kappa) v0 + d_x w0 + d_y z0
+    w = (v_x - w0)/beta,   z = (v_y - z0)/beta
+
+Discrete operators: the elliptic equation is collocated at interior nodes
+with flux continuity on edges (oracle.specelem.Mesh.collocation_matrix) and
+solved by a sparse direct LU (scipy.sparse.linalg.splu) - the plain
+definition B^{-1} F; derivatives are oracle.specelem.Mesh.grad.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse.linalg as spla
+
+from .specelem import Mesh
+
+
+class RSW:
+    """Linear rotating shallow water on the periodic unit square, state (v1, v2, eta)."""
+
+    nfields = 3
+
+    def __init__(self, mesh: Mesh, f=1.0):
+        self.mesh = mesh
+        self.f = float(f)
+        self.Gx, self.Gy = mesh.grad_matrices()
+
+    def forward(self, u):
+        """L u = (-f J v + grad eta, div v)  with J v = (v2, -v1)."""
+        v1, v2, eta = u
+        ex, ey = self.Gx @ eta, self.Gy @ eta
+        f = self.f
+        return np.stack([-f * v2 + ex, f * v1 + ey, self.Gx @ v1 + self.Gy @ v2])
+
+    def factor(self, beta):
+        m = self.mesh
+        k2 = beta * beta + self.f * self.f
+        B = m.collocation_matrix(np.full(m.NI, k2, dtype=complex))
+        return spla.splu(B)
+
+    def resolvent(self, alpha, tau, u0, lu=None):
+        """(tau L - alpha)^{-1} u0 via the elliptic reformulation."""
+        m = self.mesh
+        beta = alpha / tau
+        f = self.f
+        k2 = beta * beta + f * f
+        if lu is None:
+            lu = self.factor(beta)
+        v01, v02, eta0 = (np.asarray(c, dtype=complex) for c in u0)
+        # A_beta v0 = (beta v0 - f J v0)/(beta^2+f^2),  J v0 = (v02, -v01)
+        a1 = (beta * v01 - f * v02) / k2
+        a2 = (beta * v02 + f * v01) / k2
+        div_a = self.Gx @ a1 + self.Gy @ a2
+        F = np.zeros(m.N, dtype=complex)
+        F[: m.NI] = (k2 / beta) * (eta0[: m.NI] + div_a[: m.NI])
+        eta = lu.solve(F)
+        gx, gy = self.Gx @ eta, self.Gy @ eta
+        r1, r2 = gx - v01, gy - v02
+        v1 = (beta * r1 - f * r2) / k2
+        v2 = (beta * r2 + f * r1) / k2
+        return np.stack([v1, v2, eta]) / tau
+
+    def symbol(self, k1, k2):
+        """Fourier symbol of L on e^{2 pi i (k1 x + k2 y)} (exact, for pins)."""
+        a, b = 2j * np.pi * k1, 2j * np.pi * k2
+        f = self.f
+        return np.array([[0.0, -f, a], [f, 0.0, b], [a, b, 0.0]], dtype=complex)
+
+
+class Wave:
+    """First-order form of u_tt = kappa Lap u, state (w, z, v) = (u_x, u_y, u_t)."""
+
+    nfields = 3
+
+    def __init__(self, mesh: Mesh, kappa):
+        self.mesh = mesh
+        self.kappa = np.asarray(kappa, dtype=float)
+        if self.kappa.shape != (mesh.N,) or np.any(self.kappa <= 0):
+            raise ValueError("kappa must be positive at every global node")
+        self.Gx, self.Gy = mesh.grad_matrices()
+
+    def forward(self, u):
+        w, z, v = u
+        return np.stack([self.Gx @ v, self.Gy @ v, self.kappa * (self.Gx @ w + self.Gy @ z)])
+
+    def factor(self, beta):
+        m = self.mesh
+        B = m.collocation_matrix(beta * beta / self.kappa[: m.NI])
+        return spla.splu(B)
+
+    def resolvent(self, alpha, tau, u0, lu=None):
+        m = self.mesh
+        beta = alpha / tau
+        if lu is None:
+            lu = self.factor(beta)
+        w0, z0, v0 = (np.asarray(c, dtype=complex) for c in u0)
+        rhs = (beta / self.kappa) * v0 + self.Gx @ w0 + self.Gy @ z0
+        F = np.zeros(m.N, dtype=complex)
+        F[: m.NI] = rhs[: m.NI]
+        v = lu.solve(F)
+        w = (self.Gx @ v - w0) / beta
+        z = (self.Gy @ v - z0) / beta
+        return np.stack([w, z, v]) / tau
