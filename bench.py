@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark: repeated application of exp(tau L) ~ sum_m b_m (tau L - alpha_m)^{-1}
+ on BASELINE.json's headline configuration.
+
+A bench "step" = one big time step u <- R(tau L) u over the whole hot path
+(all half poles, leaf solves, merge sweeps, pole sum, velocity recovery).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+
+N = 1: one process.  N > 1 (torchrun): the half poles are sharded across ranks
+(pole-parallel "parallel in time"), each rank computes its
+partial pole sums and an NCCL all-reduce sums them before the velocity
+recovery ("scaling": "strong", the total work is one problem).
+--impl reference times the CPU oracle (oracle/) on a bounded sample of poles.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import CONFIGS, initial_state, wave_speed_field  # noqa: E402
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+UNIT = "dof-steps/s"
+DEFAULT_CONFIG = "c1_rsw_16x16_p16"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_problem(cfg, x, y):
+    kappa = wave_speed_field(x, y, cfg["seed"]) if cfg["model"] == "wave" else None
+    return kappa
+
+
+def roofline_for(cfg, h, times, steps, pk):
+    """Dominant kernel = the class with the largest device time.  Algorithmic work
+    per launch from DESIGN.md §6 (flops of the dense complex mat-vecs, or bytes
+    of the operators they stream)."""
+    q = cfg["p"] - 2
+    q2 = q * q
+    nelem = cfg["n"] ** 2
+    nh = h.num_half_poles
+    R2 = 2 * h.nrhs
+    shared = (cfg["model"] == "rsw")
+    dom = max(times, key=lambda k: times[k][0])
+    ms, nl = times[dom]
+    per_launch_ms = ms / max(nl, 1)
+    sm_max = pk.get("sm_max_mhz", 1965.0)
+    fp64_peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12      # TFLOP/s, FP64 FMA pipe at max clock
+    if dom == "leaf_up":
+        flops = nh * nelem * (q2 * q2 * R2 * 8 + 4 * q * q * R2 * 4)
+        bytes_ = nh * (1 if shared else nelem) * q2 * q2 * 16
+    elif dom == "leaf_down":
+        flops = nh * nelem * q2 * 4 * q * R2 * 8
+        bytes_ = nh * (1 if shared else nelem) * q2 * 4 * q * 16
+    else:
+        flops, bytes_ = None, None
+    if flops is None:
+        return {"kernel": dom, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None}
+    if shared:
+        ach = flops / (per_launch_ms * 1e-3) / 1e12
+        return {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(fp64_peak, 2),
+                "unit": "TFLOP/s", "frac": round(ach / fp64_peak, 4), "traffic": None,
+                "peak_source": "FP64 FMA pipe: 148 SMs x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md §6)",
+                "per_launch_ms": round(per_launch_ms, 4)}
+    hbm = pk.get("hbm_gbs", 6650.0)
+    ach = bytes_ / (per_launch_ms * 1e-3) / 1e9
+    return {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(ach / hbm, 4), "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+            "per_launch_ms": round(per_launch_ms, 4)}
+
+
+def oracle_sample(cfg, npoles_sample, seconds_budget=30.0):
+    """Time the CPU oracle on a bounded sample: `npoles_sample` of the poles,
+    factorization untimed (it is the setup), one resolvent apply each timed;
+    the full-step time is extrapolated by the total pole count."""
+    from oracle.models import RSW, Wave
+    from oracle.rational import build_exp_approx
+    from oracle.specelem import Mesh
+    m = Mesh(cfg["n"], cfg["p"])
+    model = RSW(m, cfg.get("f", 1.0)) if cfg["model"] == "rsw" else Wave(m, make_problem(cfg, m.x, m.y))
+    ap = build_exp_approx(cfg["Lambda_tau"], cfg["delta"], verify=False)
+    u0 = initial_state(cfg["model"], m.x, m.y, cfg["seed"])
+    P = len(ap["poles"])
+    idx = np.linspace(0, P - 1, npoles_sample).astype(int)
+    solve_s = 0.0
+    factor_s = 0.0
+    for k in idx:
+        t0 = time.perf_counter()
+        lu = model.factor(ap["poles"][k] / cfg["tau"])
+        factor_s += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        _ = ap["res"][k] * model.resolvent(ap["poles"][k], cfg["tau"], u0, lu=lu)
+        solve_s += time.perf_counter() - t0
+    step_s = solve_s / len(idx) * P
+    dof = 3 * m.N * cfg["nrhs"]
+    return {"value": dof / step_s, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{len(idx)} of {P} poles on the full {cfg['n']}x{cfg['n']}x{cfg['p']}^2 mesh, one "
+                      f"resolvent apply each (scipy splu factor untimed, {factor_s:.1f}s), step time "
+                      f"extrapolated x{P}/{len(idx)}",
+            "step_seconds": step_s}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t0 = time.perf_counter()
+    res = oracle_sample(cfg, npoles_sample=2)
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["step_seconds"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": args.config, **{k: cfg[k] for k in ("model", "n", "p", "Lambda_tau", "tau",
+                                                                      "delta", "nrhs")}},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": round(time.perf_counter() - t0, 1)}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1402_5168_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    Lam = cfg["Lambda_tau"] / cfg["tau"]
+
+    # setup (untimed): poles, factorization, device store
+    t_setup = time.perf_counter()
+    if cfg["model"] == "wave":
+        raise SystemExit("the bench workload is BASELINE config 1 (RSW); wave configs are parity cases")
+    if world > 1:
+        # shard the half poles: rank r owns a contiguous range
+        tmp = api.setup(cfg["model"], cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"],
+                        device=-1, half_range=(0, 1), nrhs=cfg["nrhs"])
+        nh_total = tmp.num_half_poles
+        tmp.close()
+        lo = nh_total * rank // world
+        hi = nh_total * (rank + 1) // world
+        h = api.setup(cfg["model"], cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"],
+                      device=local, half_range=(lo, hi), nrhs=cfg["nrhs"])
+    else:
+        h = api.setup(cfg["model"], cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"],
+                      device=local, nrhs=cfg["nrhs"])
+        nh_total = h.num_half_poles
+    t_setup = time.perf_counter() - t_setup
+    x, y = h.node_coords()
+    N = h.N
+    u0 = np.stack([initial_state(cfg["model"], x, y, cfg["seed"] + k) for k in range(cfg["nrhs"])])
+    u = torch.from_numpy(u0).to(dev).contiguous()
+    stream = torch.cuda.current_stream(dev)
+    e = torch.zeros(h.partial_len, dtype=torch.float64, device=dev) if world > 1 else None
+
+    def one_step():
+        if world == 1:
+            api.apply(h, u, 1)
+        else:
+            api.step_partial(h, u, e)
+            dist.all_reduce(e)
+            api.step_finish(h, e, u)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        api.timing_begin(h)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        ev1.record(stream)
+        ev1.synchronize()
+        kt = api.timing_end(h)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    dof = 3 * N * cfg["nrhs"]
+    value = dof * args.steps / (ms * 1e-3)
+    finite = bool(torch.isfinite(torch.view_as_real(u)).all().item())
+
+    # end-to-end through the public C ABI with HOST buffers: every step copies the
+    # state in from pinned host memory, steps, and reads it back (rexp_apply host path)
+    e2e = None
+    if world == 1:
+        uh = torch.from_numpy(u0.copy()).pin_memory()
+        uh_np = uh.numpy()
+        for _ in range(max(1, args.warmup)):
+            api.apply(h, uh_np, 1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            api.apply(h, uh_np, 1)
+        te = time.perf_counter() - t0
+        sb = u0.nbytes
+        e2e = {"value": dof * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": sb, "d2h_bytes_per_step": sb,
+               "timing": "host wall clock around K synchronous rexp_apply(host ptr, 1 step) calls"}
+
+    pk = peaks()
+    roof = roofline_for(cfg, h, kt, args.steps, pk)
+    launches = sum(v[1] for v in kt.values())
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128 (fp64)", "data": "synthetic",
+            "config": {"workload": args.config, "model": cfg["model"], "elements": f"{cfg['n']}x{cfg['n']}",
+                       "p": cfg["p"], "Lambda_tau": cfg["Lambda_tau"], "tau": cfg["tau"], "delta": cfg["delta"],
+                       "nrhs": cfg["nrhs"], "poles": h.num_poles, "half_poles_total": nh_total,
+                       "dof": dof, "nodes_per_field": N,
+                       "baseline_nodes_per_field_convention": cfg["n"] ** 2 * cfg["p"] ** 2,
+                       "store": "shared" if cfg["model"] == "rsw" else "pernode",
+                       "store_bytes": h.store_bytes, "work_bytes": h.work_bytes,
+                       "l2": "operator store + work buffers exceed the 126 MB L2 (no flush needed)",
+                       "parallelism": f"pole-sharded x{world}" if world > 1 else "single GPU"},
+            "roofline": roof,
+            "kernel_ms": {k: round(v[0], 3) for k, v in kt.items()},
+            "gpu_launches": launches, "e2e": e2e,
+            "clocks": clk.summary(), "setup_s": round(t_setup, 1), "finite": finite}
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cb = oracle_sample(cfg, npoles_sample=2)
+                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as ex:  # pragma: no cover
+                line["cpu_baseline"] = {"error": str(ex)}
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,54 @@
+"""Build librexp.so in-tree (sm_100a).  Used by __graft_entry__.build().
+
+nvcc compiles the CUDA hot path for sm_100a only; the host C++ (rational
+approximation, mesh/tree, factorization, C ABI) is compiled by g++.
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "librexp.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+
+CU = ["device.cu"]
+CPP = ["rational.cpp", "mesh.cpp", "setup_host.cpp", "api.cpp"]
+GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd):
+    print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+
+
+def build(force=False, verbose_ptxas=False):
+    os.makedirs(BUILD, exist_ok=True)
+    srcs = [os.path.join(CSRC, f) for f in CU + CPP] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".h"))]
+    srcs.append(os.path.join(os.path.dirname(HERE), "include", "rexp.h"))
+    if not force and os.path.exists(LIB):
+        t = os.path.getmtime(LIB)
+        if all(os.path.getmtime(s) <= t for s in srcs):
+            return LIB
+    objs = []
+    for f in CU:
+        o = os.path.join(BUILD, f + ".o")
+        cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c",
+               os.path.join(CSRC, f), "-o", o]
+        if verbose_ptxas:
+            cmd.insert(1, "-Xptxas=-v")
+        _run(cmd)
+        objs.append(o)
+    for f in CPP:
+        o = os.path.join(BUILD, f + ".o")
+        _run(["g++", "-O3", "-mavx2", "-mfma", "-std=c++17", "-fPIC", "-Wall", "-I", os.path.join(CUDA, "include"),
+              "-c", os.path.join(CSRC, f), "-o", o])
+        objs.append(o)
+    _run([NVCC, *GENCODE, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"])
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

@@ -1,0 +1,965 @@
+// Hot path of the rational-exponential stepper on sm_100a (B200).
+//
+// One step  u <- sum_m b_m (tau L - alpha_m)^{-1} u runs as
+//   k_pre        pole-independent RHS fields of the elliptic reformulation
+//                (§2.1: eta0, div v0, curl v0 | v0/kappa, div(w0,z0))
+//   k_leaf_up    per (half pole, leaf): f = sum_r c_r F_r, w = A_II^{-1} f, h = N_I w
+//   k_gemv X/Y   per merge level, bottom-up: w3 = Xneg (h^a_3 + h^b_3), h = h_ext + Y w3
+//   k_gemv ROOT  periodic closure s = Xroot (P^T h)
+//   k_gemv DOWN  per merge level, top-down: u3 = S u_ext + w3
+//   k_leaf_down  per (half pole, leaf): u_I = S_leaf u_B + w
+//   k_pole_sum   E_k = sum_m omega_m Re(d_mk u_m)   (conjugate pairs)
+//   k_recover    velocity recovery (Eq. "v_m, RSW" / "w and z eqns") from E
+// All poles of a level are batched into one launch (grid.y = half pole).
+// Matrices are column-major complex128; one thread owns one row (coalesced
+// 16-byte loads across a warp), columns optionally split across thread groups.
+// In the shared (translation-invariant) store one CTA applies the same matrix
+// to NB nodes, so each 16-byte load feeds NB*R2 complex FMAs.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "rexp_device.hpp"
+
+namespace rexp {
+namespace dev {
+
+__device__ __forceinline__ void cfma(double2& acc, const double2 a, const double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+
+__device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
+
+// --------------------------------------------------------------------------
+// k_pre: F[e][r][f][R2] at interior nodes
+// --------------------------------------------------------------------------
+struct PreArgs {
+    const double* u;        // state [nrhs][3][N] complex (interleaved)
+    double* F;              // [NI][nF][R2]
+    const int* elem_g;      // [nelem][p*p]
+    const double* D;        // p x p
+    const double* kappa;    // WAVE: [N]
+    int model, n, p, q, R2, nF;
+    long long N, NI;
+    double c1;              // 2/H
+};
+
+__global__ void k_pre(PreArgs a) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long total = a.NI * a.R2;
+    if (tid >= total) return;
+    const int r2 = (int)(tid % a.R2);
+    const long long g = tid / a.R2;
+    const int q2 = a.q * a.q;
+    const int e = (int)(g / q2);
+    const int rr = (int)(g % q2);
+    const int i = rr % a.q + 1, j = rr / a.q + 1;
+    const int p = a.p;
+    const int k = r2 >> 1, part = r2 & 1;
+    const double* base = a.u + (size_t)k * 3 * a.N * 2 + part;   // field fld at base + (fld*N + node)*2
+    const int* eg = a.elem_g + (size_t)e * p * p;
+    auto val = [&](int fld, int node) { return base[((size_t)fld * a.N + node) * 2]; };
+    // derivatives along the element row j (x) and column i (y)
+    double dx0 = 0, dx1 = 0, dy0 = 0, dy1 = 0;
+    for (int kk = 0; kk < p; ++kk) {
+        const double dxw = a.D[i * p + kk], dyw = a.D[j * p + kk];
+        const int gx = eg[j * p + kk], gy = eg[kk * p + i];
+        dx0 += dxw * val(0, gx);
+        dx1 += dxw * val(1, gx);
+        dy0 += dyw * val(0, gy);
+        dy1 += dyw * val(1, gy);
+    }
+    dx0 *= a.c1; dx1 *= a.c1; dy0 *= a.c1; dy1 *= a.c1;
+    double* out = a.F + ((size_t)g * a.nF) * a.R2 + r2;
+    if (a.model == 0) {  // RSW fields (v1, v2, eta): eta0, div v0, curl v0
+        out[0] = val(2, (int)g);
+        out[a.R2] = dx0 + dy1;
+        out[2 * a.R2] = dx1 - dy0;
+    } else {             // WAVE fields (w, z, v): v0/kappa, d_x w0 + d_y z0
+        out[0] = val(2, (int)g) / a.kappa[g];
+        out[a.R2] = dx0 + dy1;
+    }
+}
+
+// --------------------------------------------------------------------------
+// k_leaf_up<R2, NB>: grid (nelem/NB, nh), block rows_pad
+// --------------------------------------------------------------------------
+struct LeafUpArgs {
+    const double2* Ainv;    // [nh][nodes_stored][q2*q2] col-major
+    const double* F;        // [NI][nF][R2]
+    const double2* cF;      // [nh][nF]
+    const double* NI;       // [nb][q2] real
+    double2* w;             // [nh][nelem][q2][R2]
+    double2* h;             // [nh][hps][R2]  (leaf l, boundary b at l*nb + b)
+    long long hps;          // per-pole stride of h (in R2-vectors)
+    int q2, nb, nF, nelem, shared;
+};
+
+template <int R2, int NB>
+__global__ void __launch_bounds__(256) k_leaf_up(LeafUpArgs a) {
+    extern __shared__ double2 sm[];
+    double2* fs = sm;                               // [NB][q2][R2]
+    const int m = blockIdx.y;
+    const int leaf0 = blockIdx.x * NB;
+    const int q2 = a.q2;
+    // form the RHS f = sum_f cF[m][f] * F[f]   (complex coefficient x real field)
+    for (int t = threadIdx.x; t < NB * q2 * R2; t += blockDim.x) {
+        const int r2 = t % R2;
+        const int col = (t / R2) % q2;
+        const int lb = t / (R2 * q2);
+        const size_t g = (size_t)(leaf0 + lb) * q2 + col;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int f = 0; f < a.nF; ++f) {
+            const double v = a.F[(g * a.nF + f) * R2 + r2];
+            const double2 c = a.cF[(size_t)m * a.nF + f];
+            acc.x += c.x * v;
+            acc.y += c.y * v;
+        }
+        fs[(lb * q2 + col) * R2 + r2] = acc;
+    }
+    __syncthreads();
+    const int row = threadIdx.x;
+    double2 acc[NB][R2];
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+        for (int r = 0; r < R2; ++r) acc[lb][r] = make_double2(0.0, 0.0);
+    if (row < q2) {
+        const size_t mat = ((size_t)m * (a.shared ? 1 : a.nelem) + (a.shared ? 0 : leaf0)) * (size_t)q2 * q2;
+        const double2* M = a.Ainv + mat + row;
+        int c = 0;
+        for (; c + 4 <= q2; c += 4) {
+            double2 mv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) mv[u] = ldg2(M + (size_t)(c + u) * q2);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+                    for (int r = 0; r < R2; ++r) cfma(acc[lb][r], mv[u], fs[(lb * q2 + c + u) * R2 + r]);
+        }
+        for (; c < q2; ++c) {
+            const double2 mv = ldg2(M + (size_t)c * q2);
+#pragma unroll
+            for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+                for (int r = 0; r < R2; ++r) cfma(acc[lb][r], mv, fs[(lb * q2 + c) * R2 + r]);
+        }
+    }
+    __syncthreads();   // fs is reused for w below
+    if (row < q2) {
+#pragma unroll
+        for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+            for (int r = 0; r < R2; ++r) {
+                fs[(lb * q2 + row) * R2 + r] = acc[lb][r];
+                a.w[(((size_t)m * a.nelem + leaf0 + lb) * q2 + row) * R2 + r] = acc[lb][r];
+            }
+    }
+    __syncthreads();
+    // h = N_I w
+    for (int t = threadIdx.x; t < NB * a.nb * R2; t += blockDim.x) {
+        const int r2 = t % R2;
+        const int b = (t / R2) % a.nb;
+        const int lb = t / (R2 * a.nb);
+        double2 s = make_double2(0.0, 0.0);
+        const double* nrow = a.NI + (size_t)b * q2;
+        for (int k = 0; k < q2; ++k) {
+            const double v = __ldg(nrow + k);
+            if (v != 0.0) {
+                const double2 wv = fs[(lb * q2 + k) * R2 + r2];
+                s.x += v * wv.x;
+                s.y += v * wv.y;
+            }
+        }
+        a.h[((size_t)m * a.hps + (size_t)(leaf0 + lb) * a.nb + b) * R2 + r2] = s;
+    }
+}
+
+// --------------------------------------------------------------------------
+// generic gather-GEMV-scatter for the merge tree
+// --------------------------------------------------------------------------
+enum GemvMode { MODE_UPX = 0, MODE_UPY = 1, MODE_ROOT = 2, MODE_DOWN = 3 };
+
+struct GemvArgs {
+    const double2* M;       // [nh][nodes_stored][rows*cols] col-major
+    int rows, cols, nodes, shared;
+    int RB, CS, nrowblk;
+    // x gather
+    const double2* xsrc;    // pole-strided source
+    long long xsrc_ps;      // pole stride (in double2 of R2-vectors: elements)
+    const int* xi0;         // [nodes][cols] flat indices (or [cols] for ROOT)
+    const int* xi1;         // second term (UPX/ROOT) or null
+    // y epilogue
+    const double2* ysrc;    // additive term (UPY: child h via yi; DOWN: w3 contiguous)
+    long long ysrc_ps;
+    const int* yi;          // UPY: [nodes][rows] flat index into child h
+    double2* ydst;          // destination
+    long long ydst_ps;
+    const int* yo;          // ROOT/DOWN: scatter index [nodes][rows] or [rows]
+};
+
+template <int R2, int NB, int MODE>
+__global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
+    extern __shared__ double2 sm[];
+    const int m = blockIdx.y;
+    const int grp = blockIdx.x / a.nrowblk;
+    const int rb = blockIdx.x % a.nrowblk;
+    const int node0 = grp * NB;
+    const int cols = a.cols, rows = a.rows;
+    double2* xs = sm;                                  // [NB][cols][R2]
+    double2* red = sm + (size_t)NB * cols * R2;        // [CS][RB][NB*R2]
+    // gather x
+    const double2* src = a.xsrc + (size_t)m * a.xsrc_ps * R2;
+    for (int t = threadIdx.x; t < NB * cols * R2; t += blockDim.x) {
+        const int r2 = t % R2;
+        const int c = (t / R2) % cols;
+        const int nb = t / (R2 * cols);
+        const int node = node0 + nb;
+        double2 v;
+        if (MODE == MODE_UPX) {
+            const double2 v0 = src[(size_t)a.xi0[(size_t)node * cols + c] * R2 + r2];
+            const double2 v1 = src[(size_t)a.xi1[(size_t)node * cols + c] * R2 + r2];
+            v = make_double2(v0.x + v1.x, v0.y + v1.y);
+        } else if (MODE == MODE_UPY) {
+            v = src[((size_t)node * cols + c) * R2 + r2];
+        } else if (MODE == MODE_ROOT) {
+            const double2 v0 = src[(size_t)a.xi0[c] * R2 + r2];
+            const double2 v1 = src[(size_t)a.xi1[c] * R2 + r2];
+            v = make_double2(v0.x + v1.x, v0.y + v1.y);
+        } else {  // DOWN
+            v = src[(size_t)a.xi0[(size_t)node * cols + c] * R2 + r2];
+        }
+        xs[(nb * cols + c) * R2 + r2] = v;
+    }
+    __syncthreads();
+    const int rl = threadIdx.x % a.RB;
+    const int cs = threadIdx.x / a.RB;
+    const int row = rb * a.RB + rl;
+    double2 acc[NB][R2];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int r = 0; r < R2; ++r) acc[nb][r] = make_double2(0.0, 0.0);
+    if (row < rows && cs < a.CS) {
+        const size_t mat = ((size_t)m * (a.shared ? 1 : a.nodes) + (a.shared ? 0 : node0)) * (size_t)rows * cols;
+        const double2* M = a.M + mat + row;
+        const int CS = a.CS;
+        int c = cs;
+        for (; c + 3 * CS < cols; c += 4 * CS) {
+            double2 mv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) mv[u] = ldg2(M + (size_t)(c + u * CS) * rows);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int r = 0; r < R2; ++r) cfma(acc[nb][r], mv[u], xs[(nb * cols + c + u * CS) * R2 + r]);
+        }
+        for (; c < cols; c += CS) {
+            const double2 mv = ldg2(M + (size_t)c * rows);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                for (int r = 0; r < R2; ++r) cfma(acc[nb][r], mv, xs[(nb * cols + c) * R2 + r]);
+        }
+    }
+    if (a.CS > 1) {
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+            for (int r = 0; r < R2; ++r) red[((size_t)cs * a.RB + rl) * (NB * R2) + nb * R2 + r] = acc[nb][r];
+        __syncthreads();
+        if (cs == 0) {
+            for (int s = 1; s < a.CS; ++s)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int r = 0; r < R2; ++r) {
+                        const double2 v = red[((size_t)s * a.RB + rl) * (NB * R2) + nb * R2 + r];
+                        acc[nb][r].x += v.x;
+                        acc[nb][r].y += v.y;
+                    }
+        }
+    }
+    if (cs != 0 || row >= rows) return;
+    double2* dst = a.ydst + (size_t)m * a.ydst_ps * R2;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        const int node = node0 + nb;
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+            double2 v = acc[nb][r];
+            if (MODE == MODE_UPX) {
+                dst[((size_t)node * rows + row) * R2 + r] = v;
+            } else if (MODE == MODE_UPY) {
+                const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + (size_t)a.yi[(size_t)node * rows + row] * R2 + r];
+                v.x += add.x;
+                v.y += add.y;
+                dst[((size_t)node * rows + row) * R2 + r] = v;
+            } else if (MODE == MODE_ROOT) {
+                dst[(size_t)a.yo[row] * R2 + r] = v;
+            } else {
+                const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + ((size_t)node * rows + row) * R2 + r];
+                v.x += add.x;
+                v.y += add.y;
+                dst[(size_t)a.yo[(size_t)node * rows + row] * R2 + r] = v;
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// k_leaf_down<R2, NB>: u_I = w + S_leaf u_B (in place over w)
+// --------------------------------------------------------------------------
+struct LeafDownArgs {
+    const double2* S;       // [nh][nodes_stored][q2*nb] col-major
+    const double2* edge;    // [nh][NE][R2]
+    const int* gB;          // [nelem][nb]
+    double2* w;             // [nh][nelem][q2][R2]
+    long long NE;
+    int q2, nb, nelem, shared;
+};
+
+template <int R2, int NB>
+__global__ void __launch_bounds__(256) k_leaf_down(LeafDownArgs a) {
+    extern __shared__ double2 sm[];
+    const int m = blockIdx.y;
+    const int leaf0 = blockIdx.x * NB;
+    const int nb = a.nb, q2 = a.q2;
+    for (int t = threadIdx.x; t < NB * nb * R2; t += blockDim.x) {
+        const int r2 = t % R2;
+        const int b = (t / R2) % nb;
+        const int lb = t / (R2 * nb);
+        const int ge = a.gB[(size_t)(leaf0 + lb) * nb + b];
+        sm[(lb * nb + b) * R2 + r2] = a.edge[((size_t)m * a.NE + ge) * R2 + r2];
+    }
+    __syncthreads();
+    const int row = threadIdx.x;
+    if (row >= q2) return;
+    double2 acc[NB][R2];
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+        for (int r = 0; r < R2; ++r)
+            acc[lb][r] = a.w[(((size_t)m * a.nelem + leaf0 + lb) * q2 + row) * R2 + r];
+    const size_t mat = ((size_t)m * (a.shared ? 1 : a.nelem) + (a.shared ? 0 : leaf0)) * (size_t)q2 * nb;
+    const double2* M = a.S + mat + row;
+    int c = 0;
+    for (; c + 4 <= nb; c += 4) {
+        double2 mv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mv[u] = ldg2(M + (size_t)(c + u) * q2);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+                for (int r = 0; r < R2; ++r) cfma(acc[lb][r], mv[u], sm[(lb * nb + c + u) * R2 + r]);
+    }
+    for (; c < nb; ++c) {
+        const double2 mv = ldg2(M + (size_t)c * q2);
+#pragma unroll
+        for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+            for (int r = 0; r < R2; ++r) cfma(acc[lb][r], mv, sm[(lb * nb + c) * R2 + r]);
+    }
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+        for (int r = 0; r < R2; ++r) a.w[(((size_t)m * a.nelem + leaf0 + lb) * q2 + row) * R2 + r] = acc[lb][r];
+}
+
+// --------------------------------------------------------------------------
+// k_pole_sum: E[k][r2][g] = sum_m Re(dE[m][k] * u_m[g][r2])
+// --------------------------------------------------------------------------
+struct PoleSumArgs {
+    const double2* w;       // interior solutions [nh][NI][R2]
+    const double2* edge;    // edge solutions     [nh][NE][R2]
+    const double2* dE;      // [nh][nE]
+    double* E;              // [nE][R2][N]
+    long long N, NI, NE;
+    int nh, nE, R2;
+};
+
+__global__ void k_pole_sum(PoleSumArgs a) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (tid >= a.N * a.R2) return;
+    const long long g = tid / a.R2;
+    const int r2 = (int)(tid % a.R2);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const bool inter = g < a.NI;
+    const double2* base = inter ? (a.w + g * a.R2 + r2) : (a.edge + (g - a.NI) * a.R2 + r2);
+    const long long ps = (inter ? a.NI : a.NE) * a.R2;
+    for (int m = 0; m < a.nh; ++m) {
+        const double2 u = base[(size_t)m * ps];
+        const double2* d = a.dE + (size_t)m * a.nE;
+        const double2 d0 = d[0], d1 = d[1];
+        s0 += d0.x * u.x - d0.y * u.y;
+        s1 += d1.x * u.x - d1.y * u.y;
+        if (a.nE > 2) {
+            const double2 d2 = d[2];
+            s2 += d2.x * u.x - d2.y * u.y;
+        }
+    }
+    a.E[((size_t)0 * a.R2 + r2) * a.N + g] = s0;
+    a.E[((size_t)1 * a.R2 + r2) * a.N + g] = s1;
+    if (a.nE > 2) a.E[((size_t)2 * a.R2 + r2) * a.N + g] = s2;
+}
+
+// --------------------------------------------------------------------------
+// k_recover: new state from pole sums (velocity recovery, fused with the sum's output)
+// --------------------------------------------------------------------------
+struct RecoverArgs {
+    const double* E;        // [nE][R2][N]
+    double* u;              // state [nrhs][3][N] complex, updated in place
+    const int* elem_g;
+    const double* D;        // p x p
+    const double* Dw;       // (p-2) x p
+    int model, n, p, q, R2;
+    long long N, NI, NV;
+    double c1, s0, s1;      // RSW: P, Q ; WAVE: B1
+};
+
+__device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, long long g, double& gx, double& gy) {
+    const int p = a.p, q = a.q, n = a.n;
+    const int q2 = q * q;
+    if (g < a.NI) {
+        const int e = (int)(g / q2);
+        const int rr = (int)(g % q2);
+        const int i = rr % q + 1, j = rr / q + 1;
+        const int* eg = a.elem_g + (size_t)e * p * p;
+        double sx = 0.0, sy = 0.0;
+        for (int k = 0; k < p; ++k) {
+            sx += a.D[i * p + k] * Ef[eg[j * p + k]];
+            sy += a.D[j * p + k] * Ef[eg[k * p + i]];
+        }
+        gx = a.c1 * sx;
+        gy = a.c1 * sy;
+        return;
+    }
+    const bool vert = g < a.NI + a.NV;
+    const long long off = vert ? g - a.NI : g - a.NI - a.NV;
+    const int e = (int)(off / q);
+    const int t = (int)(off % q) + 1;   // j for vertical, i for horizontal
+    const int ex = e % n, ey = e / n;
+    auto E_of = [&](int eidx) { return a.elem_g + (size_t)eidx * p * p; };
+    if (vert) {
+        const int eL = ey * n + (ex + n - 1) % n;
+        const int* eg = E_of(e);
+        const int* egL = E_of(eL);
+        double sr = 0.0, sl = 0.0;
+        for (int k = 0; k < p; ++k) {
+            sr += a.D[0 * p + k] * Ef[eg[t * p + k]];
+            sl += a.D[(p - 1) * p + k] * Ef[egL[t * p + k]];
+        }
+        gx = 0.5 * a.c1 * (sr + sl);
+        const int eBn = ((ey + n - 1) % n) * n + ex, eTn = ((ey + 1) % n) * n + ex;
+        double st = a.Dw[(t - 1) * p + 0] * Ef[a.NI + (long long)eBn * q + (q - 1)];
+        for (int l = 1; l <= q; ++l) st += a.Dw[(t - 1) * p + l] * Ef[a.NI + (long long)e * q + (l - 1)];
+        st += a.Dw[(t - 1) * p + (p - 1)] * Ef[a.NI + (long long)eTn * q + 0];
+        gy = a.c1 * st;
+    } else {
+        const int eB = ((ey + n - 1) % n) * n + ex;
+        const int* eg = E_of(e);
+        const int* egB = E_of(eB);
+        double st_ = 0.0, sb = 0.0;
+        for (int k = 0; k < p; ++k) {
+            st_ += a.D[0 * p + k] * Ef[eg[k * p + t]];
+            sb += a.D[(p - 1) * p + k] * Ef[egB[k * p + t]];
+        }
+        gy = 0.5 * a.c1 * (st_ + sb);
+        const int eLn = ey * n + (ex + n - 1) % n, eRn = ey * n + (ex + 1) % n;
+        const long long hb = a.NI + a.NV;
+        double sx = a.Dw[(t - 1) * p + 0] * Ef[hb + (long long)eLn * q + (q - 1)];
+        for (int l = 1; l <= q; ++l) sx += a.Dw[(t - 1) * p + l] * Ef[hb + (long long)e * q + (l - 1)];
+        sx += a.Dw[(t - 1) * p + (p - 1)] * Ef[hb + (long long)eRn * q + 0];
+        gx = a.c1 * sx;
+    }
+}
+
+__global__ void k_recover(RecoverArgs a) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (tid >= a.N * a.R2) return;
+    const long long g = tid / a.R2;
+    const int r2 = (int)(tid % a.R2);
+    const int k = r2 >> 1, part = r2 & 1;
+    double* base = a.u + (size_t)k * 3 * a.N * 2 + part;
+    const double* E0 = a.E + ((size_t)0 * a.R2 + r2) * a.N;
+    const double* E1 = a.E + ((size_t)1 * a.R2 + r2) * a.N;
+    double g1x, g1y;
+    grad_at(a, E1, g, g1x, g1y);
+    if (a.model == 0) {
+        const double* E2 = a.E + ((size_t)2 * a.R2 + r2) * a.N;
+        double g2x, g2y;
+        grad_at(a, E2, g, g2x, g2y);
+        const double v1 = base[(size_t)g * 2], v2 = base[((size_t)a.N + g) * 2];
+        const double P = a.s0, Q = a.s1;
+        base[(size_t)g * 2] = g1x + g2y - P * v1 - Q * v2;
+        base[((size_t)a.N + g) * 2] = g1y - g2x - P * v2 + Q * v1;
+        base[((size_t)2 * a.N + g) * 2] = E0[g];
+    } else {
+        const double w0 = base[(size_t)g * 2], z0 = base[((size_t)a.N + g) * 2];
+        const double B1 = a.s0;
+        base[(size_t)g * 2] = g1x - B1 * w0;
+        base[((size_t)a.N + g) * 2] = g1y - B1 * z0;
+        base[((size_t)2 * a.N + g) * 2] = E0[g];
+    }
+}
+
+// ==========================================================================
+// host-side orchestration
+// ==========================================================================
+namespace {
+
+template <typename T>
+int upload(const std::vector<T>& v, T** d) {
+    *d = nullptr;
+    if (v.empty()) return REXP_OK;
+    if (cudaMalloc(d, v.size() * sizeof(T)) != cudaSuccess) return REXP_ENOMEM;
+    if (cudaMemcpy(*d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return REXP_ENODEV;
+    return REXP_OK;
+}
+
+int pick_nb(int nodes, int R2, bool shared) {
+    if (!shared) return 1;
+    int cap = 16 / R2;          // accumulators NB*R2 <= 16 complex
+    if (cap > 8) cap = 8;
+    int nb = 1;
+    while (nb * 2 <= cap && nodes % (nb * 2) == 0) nb *= 2;
+    return nb;
+}
+
+}  // namespace
+
+DeviceStore::~DeviceStore() { release(); }
+
+void DeviceStore::release() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    for (auto e : tpool) cudaEventDestroy(e);
+    tpool.clear();
+}
+
+cudaEvent_t DeviceStore::next_event() {
+    if (tpool_used == tpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        tpool.push_back(e);
+    }
+    return tpool[tpool_used++];
+}
+
+void DeviceStore::tbeg(cudaStream_t s) {
+    if (!timing) return;
+    tcur = next_event();
+    cudaEventRecord(tcur, s);
+}
+
+void DeviceStore::tend(int cls, cudaStream_t s) {
+    if (!timing) return;
+    cudaEvent_t b = next_event();
+    cudaEventRecord(b, s);
+    tlog.push_back({cls, tcur, b});
+}
+
+int DeviceStore::timing_begin() {
+    timing = true;
+    tlog.clear();
+    tpool_used = 0;
+    return REXP_OK;
+}
+
+int DeviceStore::timing_end(double* ms, int32_t* launches) {
+    timing = false;
+    for (int k = 0; k < T_NCLASS; ++k) {
+        if (ms) ms[k] = 0.0;
+        if (launches) launches[k] = 0;
+    }
+    if (!tlog.empty() && cudaEventSynchronize(tlog.back().b) != cudaSuccess) return check("timing_end");
+    for (auto& t : tlog) {
+        float x = 0.f;
+        cudaEventElapsedTime(&x, t.a, t.b);
+        if (ms) ms[t.cls] += x;
+        if (launches) launches[t.cls] += 1;
+    }
+    tlog.clear();
+    tpool_used = 0;
+    return check("timing_end");
+}
+
+template <typename T>
+int DeviceStore::alloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) return REXP_OK;
+    if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) {
+        set_error("cudaMalloc failed (" + std::to_string(count * sizeof(T)) + " bytes)");
+        return REXP_ENOMEM;
+    }
+    allocs.push_back(*p);
+    return REXP_OK;
+}
+
+template <typename T>
+int DeviceStore::put(T** p, const std::vector<T>& v) {
+    int rc = alloc(p, v.size());
+    if (rc) return rc;
+    if (!v.empty() && cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error("cudaMemcpy H2D failed");
+        return REXP_ENODEV;
+    }
+    return REXP_OK;
+}
+
+int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int h0_, int h1_, bool shared_,
+                      int nrhs_, const std::vector<HostLevelOps>& ops) {
+    model = P.model;
+    n = T.n; p = T.p; q = T.q; q2 = q * q; nb = 4 * q;
+    N = T.N; NI = T.NI; NV = T.NV; NE = T.NE; nelem = T.nelem;
+    h0 = h0_; h1 = h1_; nh = h1 - h0;
+    shared = shared_;
+    nrhs = nrhs_;
+    R2 = 2 * nrhs;
+    nF = pt.nF;
+    nE = pt.nE;
+    c1 = 2.0 * n;
+    scal = pt.scal;
+    int rc;
+    // mesh data
+    const Cheb ch = make_cheb(p);
+    if ((rc = put(&d_D, ch.D))) return rc;
+    if ((rc = put(&d_Dw, ch.Dw))) return rc;
+    if ((rc = put(&d_elem_g, T.elem_g))) return rc;
+    if (model == REXP_MODEL_WAVE) {
+        if ((rc = put(&d_kappa, P.kappa))) return rc;
+    }
+    // N_I (pole independent, real): recompute from the leaf geometry
+    {
+        std::vector<double> NIm(static_cast<size_t>(nb) * q2, 0.0);
+        const double* D = ch.D.data();
+        auto I = [this](int i, int j) { return (j - 1) * q + (i - 1); };
+        for (int i = 1; i <= q; ++i)
+            for (int k = 1; k <= p - 2; ++k) {
+                NIm[static_cast<size_t>(i - 1) * q2 + I(i, k)] += -c1 * D[0 * p + k];               // bottom
+                NIm[static_cast<size_t>(2 * q + i - 1) * q2 + I(i, k)] += c1 * D[(p - 1) * p + k];  // top
+            }
+        for (int j = 1; j <= q; ++j)
+            for (int k = 1; k <= p - 2; ++k) {
+                NIm[static_cast<size_t>(q + j - 1) * q2 + I(k, j)] += c1 * D[(p - 1) * p + k];      // right
+                NIm[static_cast<size_t>(3 * q + j - 1) * q2 + I(k, j)] += -c1 * D[0 * p + k];       // left
+            }
+        if ((rc = put(&d_NI, NIm))) return rc;
+    }
+    // pole tables for this handle's range
+    {
+        std::vector<double2> cF(static_cast<size_t>(nh) * nF), dE(static_cast<size_t>(nh) * nE);
+        for (int m = 0; m < nh; ++m) {
+            for (int f = 0; f < nF; ++f) {
+                const cd v = pt.cF[static_cast<size_t>(h0 + m) * nF + f];
+                cF[static_cast<size_t>(m) * nF + f] = make_double2(v.real(), v.imag());
+            }
+            for (int k = 0; k < nE; ++k) {
+                const cd v = pt.dE[static_cast<size_t>(h0 + m) * nE + k];
+                dE[static_cast<size_t>(m) * nE + k] = make_double2(v.real(), v.imag());
+            }
+        }
+        if ((rc = put(&d_cF, cF))) return rc;
+        if ((rc = put(&d_dE, dE))) return rc;
+    }
+    // operators
+    store_bytes = 0;
+    auto put_ops = [&](const std::vector<cd>& v, double2** d) -> int {
+        std::vector<double2> tmp(v.size());
+        for (size_t k = 0; k < v.size(); ++k) tmp[k] = make_double2(v[k].real(), v[k].imag());
+        store_bytes += static_cast<int64_t>(v.size()) * 16;
+        return put(d, tmp);
+    };
+    if ((rc = put_ops(ops[0].m[0], &d_Ainv))) return rc;
+    if ((rc = put_ops(ops[0].m[1], &d_Sleaf))) return rc;
+    if ((rc = put(&d_leaf_gB, T.leaf_gB))) return rc;
+    levels.resize(T.levels.size());
+    for (size_t li = 0; li < T.levels.size(); ++li) {
+        const MergeLevel& L = T.levels[li];
+        Level& D = levels[li];
+        D.nodes = L.nodes; D.n3 = L.n3; D.next = L.next; D.nchild = L.nchild; D.child_nodes = L.child_nodes;
+        if ((rc = put_ops(ops[li + 1].m[0], &D.X))) return rc;
+        if ((rc = put_ops(ops[li + 1].m[1], &D.Y))) return rc;
+        if ((rc = put_ops(ops[li + 1].m[2], &D.S))) return rc;
+        if ((rc = put(&D.ia3, L.ia3))) return rc;
+        if ((rc = put(&D.ib3, L.ib3))) return rc;
+        if ((rc = put(&D.ext, L.ext))) return rc;
+        if ((rc = put(&D.gext, L.gext))) return rc;
+        if ((rc = put(&D.g3, L.g3))) return rc;
+    }
+    ns = T.ns;
+    nroot_b = 4 * T.n * T.q;
+    if ((rc = put_ops(ops.back().m[0], &d_Xroot))) return rc;
+    if ((rc = put(&d_rpos1, T.root_pos1))) return rc;
+    if ((rc = put(&d_rpos2, T.root_pos2))) return rc;
+    if ((rc = put(&d_rgs, T.root_gs))) return rc;
+    // work buffers
+    work_bytes = 0;
+    auto walloc = [&](auto** pp, size_t count, size_t elt) -> int {
+        work_bytes += static_cast<int64_t>(count * elt);
+        return alloc(pp, count);
+    };
+    if ((rc = walloc(&d_F, static_cast<size_t>(NI) * nF * R2, 8))) return rc;
+    if ((rc = walloc(&d_w, static_cast<size_t>(nh) * NI * R2, 16))) return rc;
+    if ((rc = walloc(&d_edge, static_cast<size_t>(nh) * NE * R2, 16))) return rc;
+    size_t hmax = static_cast<size_t>(nelem) * nb;
+    for (auto& L : T.levels) hmax = std::max(hmax, static_cast<size_t>(L.nodes) * L.next);
+    if ((rc = walloc(&d_h[0], static_cast<size_t>(nh) * hmax * R2, 16))) return rc;
+    if ((rc = walloc(&d_h[1], static_cast<size_t>(nh) * hmax * R2, 16))) return rc;
+    hstride = static_cast<long long>(hmax);
+    for (size_t li = 0; li < levels.size(); ++li) {
+        Level& D = levels[li];
+        if ((rc = walloc(&D.w3, static_cast<size_t>(nh) * D.nodes * D.n3 * R2, 16))) return rc;
+    }
+    if ((rc = walloc(&d_E, static_cast<size_t>(nE) * R2 * N, 8))) return rc;
+    if ((rc = walloc(&d_u, static_cast<size_t>(nrhs) * 3 * N * 2, 8))) return rc;
+    // allow large dynamic shared memory on the templated kernels
+    configure_kernels();
+    return REXP_OK;
+}
+
+// launch helpers -------------------------------------------------------------
+namespace {
+
+template <int R2>
+void launch_leaf_up_nb(int NB, dim3 grid, int threads, size_t smem, cudaStream_t s, const LeafUpArgs& a) {
+    switch (NB) {
+        case 1: k_leaf_up<R2, 1><<<grid, threads, smem, s>>>(a); break;
+        case 2: k_leaf_up<R2, 2><<<grid, threads, smem, s>>>(a); break;
+        case 4: k_leaf_up<R2, 4><<<grid, threads, smem, s>>>(a); break;
+        default: k_leaf_up<R2, 8><<<grid, threads, smem, s>>>(a); break;
+    }
+}
+template <int R2>
+void launch_leaf_down_nb(int NB, dim3 grid, int threads, size_t smem, cudaStream_t s, const LeafDownArgs& a) {
+    switch (NB) {
+        case 1: k_leaf_down<R2, 1><<<grid, threads, smem, s>>>(a); break;
+        case 2: k_leaf_down<R2, 2><<<grid, threads, smem, s>>>(a); break;
+        case 4: k_leaf_down<R2, 4><<<grid, threads, smem, s>>>(a); break;
+        default: k_leaf_down<R2, 8><<<grid, threads, smem, s>>>(a); break;
+    }
+}
+template <int R2, int MODE>
+void launch_gemv_nb(int NB, dim3 grid, size_t smem, cudaStream_t s, const GemvArgs& a) {
+    switch (NB) {
+        case 1: k_gemv<R2, 1, MODE><<<grid, 256, smem, s>>>(a); break;
+        case 2: k_gemv<R2, 2, MODE><<<grid, 256, smem, s>>>(a); break;
+        case 4: k_gemv<R2, 4, MODE><<<grid, 256, smem, s>>>(a); break;
+        default: k_gemv<R2, 8, MODE><<<grid, 256, smem, s>>>(a); break;
+    }
+}
+template <int MODE>
+void launch_gemv(int R2, int NB, dim3 grid, size_t smem, cudaStream_t s, const GemvArgs& a) {
+    switch (R2) {
+        case 2: launch_gemv_nb<2, MODE>(NB, grid, smem, s, a); break;
+        case 4: launch_gemv_nb<4, MODE>(NB, grid, smem, s, a); break;
+        default: launch_gemv_nb<8, MODE>(NB, grid, smem, s, a); break;
+    }
+}
+
+template <typename K>
+void allow_smem(K kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+template <int R2, int NB>
+void allow_all_nb() {
+    allow_smem(k_leaf_up<R2, NB>);
+    allow_smem(k_leaf_down<R2, NB>);
+    allow_smem(k_gemv<R2, NB, MODE_UPX>);
+    allow_smem(k_gemv<R2, NB, MODE_UPY>);
+    allow_smem(k_gemv<R2, NB, MODE_ROOT>);
+    allow_smem(k_gemv<R2, NB, MODE_DOWN>);
+}
+template <int R2>
+void allow_all() {
+    allow_all_nb<R2, 1>();
+    allow_all_nb<R2, 2>();
+    allow_all_nb<R2, 4>();
+    allow_all_nb<R2, 8>();
+}
+
+GemvArgs gemv_shape(int rows, int cols, int nodes, bool shared) {
+    GemvArgs g{};
+    g.rows = rows;
+    g.cols = cols;
+    g.nodes = nodes;
+    g.shared = shared ? 1 : 0;
+    int rb = ((rows + 31) / 32) * 32;
+    if (rb > 256) rb = 256;
+    g.RB = rb;
+    g.CS = 256 / rb;
+    if (g.CS > 8) g.CS = 8;
+    g.nrowblk = (rows + rb - 1) / rb;
+    return g;
+}
+
+size_t gemv_smem(const GemvArgs& g, int NB, int R2) {
+    return (static_cast<size_t>(NB) * g.cols * R2 + static_cast<size_t>(g.CS > 1 ? g.CS : 0) * g.RB * NB * R2) *
+           sizeof(double2);
+}
+
+}  // namespace
+
+void DeviceStore::configure_kernels() {
+    allow_all<2>();
+    allow_all<4>();
+    allow_all<8>();
+}
+
+int DeviceStore::launches_per_step() const { return 6 + 3 * static_cast<int>(levels.size()); }
+
+int DeviceStore::check(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(what) + ": " + cudaGetErrorString(e));
+        return REXP_ENODEV;
+    }
+    return REXP_OK;
+}
+
+// Solve all half poles of this handle for the state in d_state (up to leaf_down).
+int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
+    // pre
+    {
+        PreArgs a{};
+        a.u = d_state; a.F = d_F; a.elem_g = d_elem_g; a.D = d_D; a.kappa = d_kappa;
+        a.model = model; a.n = n; a.p = p; a.q = q; a.R2 = R2; a.nF = nF; a.N = N; a.NI = NI; a.c1 = c1;
+        const long long tot = NI * R2;
+        tbeg(s);
+        k_pre<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
+        tend(T_PRE, s);
+    }
+    // leaves up
+    const int NBl = pick_nb(nelem, R2, shared);
+    const int thr = ((q2 + 31) / 32) * 32;
+    {
+        LeafUpArgs a{};
+        a.Ainv = d_Ainv; a.F = d_F; a.cF = d_cF; a.NI = d_NI; a.w = d_w; a.h = d_h[0]; a.hps = hstride;
+        a.q2 = q2; a.nb = nb; a.nF = nF; a.nelem = nelem; a.shared = shared ? 1 : 0;
+        dim3 grid(nelem / NBl, nh);
+        const size_t smem = static_cast<size_t>(NBl) * q2 * R2 * sizeof(double2);
+        tbeg(s);
+        switch (R2) {
+            case 2: launch_leaf_up_nb<2>(NBl, grid, thr, smem, s, a); break;
+            case 4: launch_leaf_up_nb<4>(NBl, grid, thr, smem, s, a); break;
+            default: launch_leaf_up_nb<8>(NBl, grid, thr, smem, s, a); break;
+        }
+        tend(T_LEAF_UP, s);
+    }
+    // NOTE: h per pole is stored with stride hstride (elements of R2-vectors)
+    // merges up
+    for (size_t li = 0; li < levels.size(); ++li) {
+        Level& L = levels[li];
+        const double2* hc = d_h[li % 2];
+        double2* hp = d_h[(li + 1) % 2];
+        const int NB = pick_nb(L.nodes, R2, shared);
+        {  // X stage
+            GemvArgs g = gemv_shape(L.n3, L.n3, L.nodes, shared);
+            g.M = L.X; g.xsrc = hc; g.xsrc_ps = hstride; g.xi0 = L.ia3; g.xi1 = L.ib3;
+            g.ydst = L.w3; g.ydst_ps = static_cast<long long>(L.nodes) * L.n3;
+            dim3 grid((L.nodes / NB) * g.nrowblk, nh);
+            tbeg(s);
+            launch_gemv<MODE_UPX>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
+            tend(T_MERGE_UP, s);
+        }
+        {  // Y stage
+            GemvArgs g = gemv_shape(L.next, L.n3, L.nodes, shared);
+            g.M = L.Y; g.xsrc = L.w3; g.xsrc_ps = static_cast<long long>(L.nodes) * L.n3;
+            g.ysrc = hc; g.ysrc_ps = hstride; g.yi = L.ext;
+            g.ydst = hp; g.ydst_ps = hstride;
+            dim3 grid((L.nodes / NB) * g.nrowblk, nh);
+            tbeg(s);
+            launch_gemv<MODE_UPY>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
+            tend(T_MERGE_UP, s);
+        }
+    }
+    // root closure
+    {
+        const double2* hr = d_h[levels.size() % 2];
+        GemvArgs g = gemv_shape(ns, ns, 1, true);
+        g.shared = 1;
+        g.M = d_Xroot; g.xsrc = hr; g.xsrc_ps = hstride; g.xi0 = d_rpos1; g.xi1 = d_rpos2;
+        g.ydst = d_edge; g.ydst_ps = NE; g.yo = d_rgs;
+        dim3 grid(g.nrowblk, nh);
+        tbeg(s);
+        launch_gemv<MODE_ROOT>(R2, 1, grid, gemv_smem(g, 1, R2), s, g);
+        tend(T_ROOT, s);
+    }
+    // merges down
+    for (int li = static_cast<int>(levels.size()) - 1; li >= 0; --li) {
+        Level& L = levels[li];
+        const int NB = pick_nb(L.nodes, R2, shared);
+        GemvArgs g = gemv_shape(L.n3, L.next, L.nodes, shared);
+        g.M = L.S; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
+        g.ysrc = L.w3; g.ysrc_ps = static_cast<long long>(L.nodes) * L.n3;
+        g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
+        dim3 grid((L.nodes / NB) * g.nrowblk, nh);
+        tbeg(s);
+        launch_gemv<MODE_DOWN>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
+        tend(T_MERGE_DOWN, s);
+    }
+    // leaves down
+    {
+        LeafDownArgs a{};
+        a.S = d_Sleaf; a.edge = d_edge; a.gB = d_leaf_gB; a.w = d_w; a.NE = NE;
+        a.q2 = q2; a.nb = nb; a.nelem = nelem; a.shared = shared ? 1 : 0;
+        dim3 grid(nelem / NBl, nh);
+        const size_t smem = static_cast<size_t>(NBl) * nb * R2 * sizeof(double2);
+        tbeg(s);
+        switch (R2) {
+            case 2: launch_leaf_down_nb<2>(NBl, grid, thr, smem, s, a); break;
+            case 4: launch_leaf_down_nb<4>(NBl, grid, thr, smem, s, a); break;
+            default: launch_leaf_down_nb<8>(NBl, grid, thr, smem, s, a); break;
+        }
+        tend(T_LEAF_DOWN, s);
+    }
+    return check("solve_poles");
+}
+
+int DeviceStore::pole_sum(double* d_E_out, cudaStream_t s) {
+    PoleSumArgs a{};
+    a.w = d_w; a.edge = d_edge; a.dE = d_dE; a.E = d_E_out;
+    a.N = N; a.NI = NI; a.NE = NE; a.nh = nh; a.nE = nE; a.R2 = R2;
+    const long long tot = N * R2;
+    tbeg(s);
+    k_pole_sum<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
+    tend(T_POLE_SUM, s);
+    return check("pole_sum");
+}
+
+int DeviceStore::recover(const double* d_E_in, double* d_state, cudaStream_t s) {
+    RecoverArgs a{};
+    a.E = d_E_in; a.u = d_state; a.elem_g = d_elem_g; a.D = d_D; a.Dw = d_Dw;
+    a.model = model; a.n = n; a.p = p; a.q = q; a.R2 = R2; a.N = N; a.NI = NI; a.NV = NV; a.c1 = c1;
+    a.s0 = scal.size() > 0 ? scal[0] : 0.0;
+    a.s1 = scal.size() > 1 ? scal[1] : 0.0;
+    const long long tot = N * R2;
+    tbeg(s);
+    k_recover<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
+    tend(T_RECOVER, s);
+    return check("recover");
+}
+
+int DeviceStore::step(double* d_state, cudaStream_t s) {
+    int rc = solve_poles(d_state, s);
+    if (rc) return rc;
+    if ((rc = pole_sum(d_E, s))) return rc;
+    return recover(d_E, d_state, s);
+}
+
+
+}  // namespace dev
+}  // namespace rexp

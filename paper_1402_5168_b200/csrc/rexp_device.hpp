@@ -1,0 +1,78 @@
+// Device operator store and hot-path launcher (see device.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "rexp_internal.hpp"
+
+namespace rexp {
+namespace dev {
+
+struct Level {
+    int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0;
+    double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
+    int *ia3 = nullptr, *ib3 = nullptr, *ext = nullptr, *gext = nullptr, *g3 = nullptr;
+    double2* w3 = nullptr;                              // [nh][nodes][n3][R2]
+};
+
+class DeviceStore {
+  public:
+    ~DeviceStore();
+    int init(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1, bool shared, int nrhs,
+             const std::vector<HostLevelOps>& ops);
+    void release();
+    // one full step on a device state [nrhs][3][N] complex128
+    int step(double* d_state, cudaStream_t s);
+    int solve_poles(const double* d_state, cudaStream_t s);
+    int pole_sum(double* d_E_out, cudaStream_t s);
+    int recover(const double* d_E_in, double* d_state, cudaStream_t s);
+    int launches_per_step() const;
+
+    // per-kernel-class CUDA-event timing on the launching stream
+    enum { T_PRE = 0, T_LEAF_UP, T_MERGE_UP, T_ROOT, T_MERGE_DOWN, T_LEAF_DOWN, T_POLE_SUM, T_RECOVER, T_NCLASS };
+    int timing_begin();
+    int timing_end(double* ms, int32_t* launches);
+
+    int model = 0, n = 0, p = 0, q = 0, q2 = 0, nb = 0, nelem = 0;
+    long long N = 0, NI = 0, NV = 0, NE = 0;
+    int h0 = 0, h1 = 0, nh = 0, nrhs = 1, R2 = 2, nF = 0, nE = 0, ns = 0, nroot_b = 0;
+    bool shared = true;
+    double c1 = 0.0;
+    std::vector<double> scal;
+    int64_t store_bytes = 0, work_bytes = 0;
+    double* d_u = nullptr;     // device state buffer for host-pointer applies
+    double* d_E = nullptr;     // pole sums [nE][R2][N]
+
+  private:
+    template <typename T>
+    int alloc(T** p, size_t count);
+    template <typename T>
+    int put(T** p, const std::vector<T>& v);
+    int check(const char* what);
+    void configure_kernels();
+
+    void tbeg(cudaStream_t s);
+    void tend(int cls, cudaStream_t s);
+    bool timing = false;
+    struct TEntry { int cls; cudaEvent_t a, b; };
+    std::vector<TEntry> tlog;
+    std::vector<cudaEvent_t> tpool;
+    size_t tpool_used = 0;
+    cudaEvent_t tcur = nullptr;
+    cudaEvent_t next_event();
+
+    std::vector<void*> allocs;
+    double *d_D = nullptr, *d_Dw = nullptr, *d_kappa = nullptr, *d_NI = nullptr, *d_F = nullptr;
+    int *d_elem_g = nullptr, *d_leaf_gB = nullptr, *d_rpos1 = nullptr, *d_rpos2 = nullptr, *d_rgs = nullptr;
+    double2 *d_cF = nullptr, *d_dE = nullptr;
+    double2 *d_Ainv = nullptr, *d_Sleaf = nullptr, *d_Xroot = nullptr;
+    double2 *d_w = nullptr, *d_edge = nullptr;
+    double2* d_h[2] = {nullptr, nullptr};
+    long long hstride = 0;
+    std::vector<Level> levels;
+};
+
+}  // namespace dev
+}  // namespace rexp

@@ -1,0 +1,206 @@
+"""CPU checks of librexp's host-side build stage (no GPU needed).
+
+* the library loads and exports every symbol include/rexp.h declares;
+* poles/weights agree with the oracle's construction of PAPER.md §3;
+* node ordering/coordinates agree with the oracle mesh;
+* the exported merge-tree operators, applied with the HPS recurrences
+  (written out here in numpy, as test infrastructure), reproduce the oracle's
+  sparse direct solve of the collocation system (§2.2-2.3) for
+  single poles - i.e. the factorization is exact up to rounding.
+"""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from oracle.rational import build_exp_approx
+from oracle.specelem import Mesh
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_1402_5168_b200 import _lib
+    return _lib
+
+
+def test_header_symbols_exported():
+    lib = _lib().load()
+    hdr = open(os.path.join(ROOT, "include", "rexp.h")).read()
+    names = set(re.findall(r"\b(rexp_[a-z_]+)\s*\(", hdr))
+    names = {n for n in names if n not in ("rexp_problem", "rexp_options", "rexp_handle")}
+    assert len(names) >= 18
+    declared_in_binding = {s[0] for s in _lib().SIGNATURES}
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in declared_in_binding, n
+
+
+@pytest.fixture(scope="module")
+def host_rsw():
+    from paper_1402_5168_b200 import api
+    return api.setup("rsw", n=4, p=8, tau=0.2, delta=1e-10, Lambda=100.0, f=1.0, device=-1, store="pernode")
+
+
+def test_poles_match_oracle(host_rsw):
+    a, b = host_rsw.poles()
+    ref = build_exp_approx(20.0, 1e-10)
+    assert len(a) == len(ref["poles"])
+    assert np.abs(a - ref["poles"]).max() < 1e-12 * np.abs(ref["poles"]).max()
+    assert np.abs(b - ref["res"]).max() < 1e-11 * np.abs(ref["res"]).max()
+    err, mx = host_rsw.accuracy()
+    assert err <= 1e-10 and mx <= 1 + 1e-10
+    # half poles: Im(alpha) >= 0
+    assert host_rsw.num_half_poles == int(np.sum(ref["poles"].imag >= 0))
+
+
+def test_node_coords_match_oracle(host_rsw):
+    x, y = host_rsw.node_coords()
+    m = Mesh(4, 8)
+    assert np.abs(x - m.x).max() < 1e-15 and np.abs(y - m.y).max() < 1e-15
+
+
+def _hps_apply(api, h, half, f_int, NI_mat, n, p):
+    """Numpy transcription of the HPS solve recurrences on the exported operators."""
+    q = p - 2
+    q2, nb = q * q, 4 * q
+    nlev = api.export_num_levels(h)
+    info0 = api.export_level_info(h, 0)
+    nelem = info0[0]
+    shared0 = info0[1] == 1
+    gB = api.export_index(h, 0, 3, nelem * nb).reshape(nelem, nb)
+    NE = 2 * nelem * q
+    w = np.zeros((nelem, q2), complex)
+    hbuf = np.zeros((nelem, nb), complex)
+    for e in range(nelem):
+        A = api.export_matrix(h, half, 0, 0 if shared0 else e, 0, q2, q2)
+        w[e] = A @ f_int[e]
+        hbuf[e] = NI_mat @ w[e]
+    hprev = hbuf.reshape(-1)
+    w3s = []
+    for lev in range(1, nlev - 1):
+        info = api.export_level_info(h, lev)
+        nodes, stored, n3, ne, nc = info[:5]
+        ia3 = api.export_index(h, lev, 0, nodes * n3).reshape(nodes, n3)
+        ib3 = api.export_index(h, lev, 1, nodes * n3).reshape(nodes, n3)
+        ext = api.export_index(h, lev, 2, nodes * ne).reshape(nodes, ne)
+        hnew = np.zeros((nodes, ne), complex)
+        w3 = np.zeros((nodes, n3), complex)
+        for nd in range(nodes):
+            k = 0 if stored == 1 else nd
+            X = api.export_matrix(h, half, lev, k, 0, n3, n3)
+            Y = api.export_matrix(h, half, lev, k, 1, ne, n3)
+            w3[nd] = X @ (hprev[ia3[nd]] + hprev[ib3[nd]])
+            hnew[nd] = hprev[ext[nd]] + Y @ w3[nd]
+        w3s.append(w3)
+        hprev = hnew.reshape(-1)
+    info = api.export_level_info(h, nlev - 1)
+    ns = info[2]
+    p1 = api.export_index(h, nlev - 1, 0, ns)
+    p2 = api.export_index(h, nlev - 1, 1, ns)
+    gs = api.export_index(h, nlev - 1, 2, ns)
+    Xr = api.export_matrix(h, half, nlev - 1, 0, 0, ns, ns)
+    edge = np.zeros(NE, complex)
+    edge[gs] = Xr @ (hprev[p1] + hprev[p2])
+    for lev in range(nlev - 2, 0, -1):
+        info = api.export_level_info(h, lev)
+        nodes, stored, n3, ne = info[:4]
+        gext = api.export_index(h, lev, 3, nodes * ne).reshape(nodes, ne)
+        g3 = api.export_index(h, lev, 4, nodes * n3).reshape(nodes, n3)
+        for nd in range(nodes):
+            k = 0 if stored == 1 else nd
+            S = api.export_matrix(h, half, lev, k, 2, n3, ne)
+            edge[g3[nd]] = S @ edge[gext[nd]] + w3s[lev - 1][nd]
+    uI = np.zeros((nelem, q2), complex)
+    for e in range(nelem):
+        S = api.export_matrix(h, half, 0, 0 if shared0 else e, 1, q2, nb)
+        uI[e] = S @ edge[gB[e]] + w[e]
+    return np.concatenate([uI.reshape(-1), edge])
+
+
+def _leaf_flux_matrix(m):
+    """N_I: outward normal derivative at leaf boundary nodes from interior values."""
+    p, q = m.p, m.q
+    c1 = 2.0 / m.H
+    D = m.D
+    NI = np.zeros((4 * q, q * q))
+    I = lambda i, j: (j - 1) * q + (i - 1)
+    for i in range(1, q + 1):
+        for k in range(1, p - 1):
+            NI[i - 1, I(i, k)] += -c1 * D[0, k]
+            NI[2 * q + i - 1, I(i, k)] += c1 * D[p - 1, k]
+    for j in range(1, q + 1):
+        for k in range(1, p - 1):
+            NI[q + j - 1, I(k, j)] += c1 * D[p - 1, k]
+            NI[3 * q + j - 1, I(k, j)] += -c1 * D[0, k]
+    return NI
+
+
+@pytest.mark.parametrize("store", ["pernode", "shared"])
+def test_hps_operators_reproduce_sparse_solve_rsw(store):
+    from paper_1402_5168_b200 import api
+    n, p, tau, f = 4, 8, 0.2, 1.0
+    h = api.setup("rsw", n=n, p=p, tau=tau, delta=1e-10, Lambda=100.0, f=f, device=-1, store=store)
+    m = Mesh(n, p)
+    NI_mat = _leaf_flux_matrix(m)
+    a, _ = h.poles()
+    half_alpha = a[a.imag >= 0]
+    rng = np.random.default_rng(0)
+    F = rng.standard_normal(m.NI) + 1j * rng.standard_normal(m.NI)
+    for half in [0, 7, h.num_half_poles // 2, h.num_half_poles - 1]:
+        beta = half_alpha[half] / tau
+        k2 = beta * beta + f * f
+        B = m.collocation_matrix(np.full(m.NI, k2))
+        rhs = np.zeros(m.N, complex)
+        rhs[: m.NI] = F
+        ref = spla.splu(B).solve(rhs)
+        got = _hps_apply(api, h, half, F.reshape(n * n, -1), NI_mat, n, p)
+        assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max(), (half, np.abs(got - ref).max())
+    h.close()
+
+
+def test_hps_operators_reproduce_sparse_solve_wave():
+    from paper_1402_5168_b200 import api
+    from workloads import wave_speed_field
+    n, p, tau = 4, 8, 0.2
+    m = Mesh(n, p)
+    kappa = wave_speed_field(m.x, m.y, seed=3)
+    h = api.setup("wave", n=n, p=p, tau=tau, delta=1e-10, Lambda=100.0, kappa=kappa, device=-1)
+    NI_mat = _leaf_flux_matrix(m)
+    a, _ = h.poles()
+    half_alpha = a[a.imag >= 0]
+    rng = np.random.default_rng(1)
+    F = rng.standard_normal(m.NI) + 1j * rng.standard_normal(m.NI)
+    for half in [1, h.num_half_poles - 3]:
+        beta = half_alpha[half] / tau
+        B = m.collocation_matrix(beta * beta / kappa[: m.NI])
+        rhs = np.zeros(m.N, complex)
+        rhs[: m.NI] = F
+        ref = spla.splu(B).solve(rhs)
+        got = _hps_apply(api, h, half, F.reshape(n * n, -1), NI_mat, n, p)
+        assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max()
+    h.close()
+
+
+def test_setup_rejects_bad_arguments():
+    from paper_1402_5168_b200 import api
+    from paper_1402_5168_b200._lib import RexpError
+    with pytest.raises(RexpError):
+        api.setup("rsw", n=3, p=8, tau=0.2, delta=1e-10, Lambda=100.0, device=-1)
+    with pytest.raises(RexpError):
+        api.setup("rsw", n=4, p=8, tau=0.2, delta=1e-16, Lambda=100.0, device=-1)
+    with pytest.raises(RexpError):
+        api.setup("wave", n=4, p=8, tau=0.2, delta=1e-10, Lambda=100.0, device=-1)  # no kappa
+
+
+def test_device_setup_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1402_5168_b200 import api
+    from paper_1402_5168_b200._lib import RexpError
+    with pytest.raises(RexpError, match="CUDA|device"):
+        api.setup("rsw", n=2, p=6, tau=0.2, delta=1e-10, Lambda=50.0, device=0)
