@@ -94,11 +94,12 @@ struct LeafUpArgs {
     const double2* Ainv;    // [nh][nodes_stored][q2*q2] col-major
     const double* F;        // [NI][nF][R2]
     const double2* cF;      // [nh][nF]
-    const double* NI;       // [nb][q2] real
+    const double* D;        // p x p differentiation matrix
+    double c1;              // 2/H
     double2* w;             // [nh][nelem][q2][R2]
     double2* h;             // [nh][hps][R2]  (leaf l, boundary b at l*nb + b)
     long long hps;          // per-pole stride of h (in R2-vectors)
-    int q2, nb, nF, nelem, shared;
+    int q, q2, nb, nF, nelem, shared;
 };
 
 template <int R2, int NB>
@@ -164,22 +165,25 @@ __global__ void __launch_bounds__(256) k_leaf_up(LeafUpArgs a) {
             }
     }
     __syncthreads();
-    // h = N_I w
+    // h = N_I w: outward normal derivative of the particular solution at the leaf
+    // boundary (bottom, right, top, left); each is a q-term sum along one grid line.
+    const int q = a.q, p = q + 2;
     for (int t = threadIdx.x; t < NB * a.nb * R2; t += blockDim.x) {
         const int r2 = t % R2;
         const int b = (t / R2) % a.nb;
         const int lb = t / (R2 * a.nb);
+        const int side = b / q, s1 = b % q;   // s1 = i-1 (bottom/top) or j-1 (right/left)
+        const double* drow = a.D + (side == 0 || side == 3 ? 0 : (p - 1) * p);
+        const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
         double2 s = make_double2(0.0, 0.0);
-        const double* nrow = a.NI + (size_t)b * q2;
-        for (int k = 0; k < q2; ++k) {
-            const double v = __ldg(nrow + k);
-            if (v != 0.0) {
-                const double2 wv = fs[(lb * q2 + k) * R2 + r2];
-                s.x += v * wv.x;
-                s.y += v * wv.y;
-            }
+        for (int k = 1; k <= q; ++k) {
+            const int idx = (side == 0 || side == 2) ? (k - 1) * q + s1 : s1 * q + (k - 1);
+            const double v = __ldg(drow + k);
+            const double2 wv = fs[(lb * q2 + idx) * R2 + r2];
+            s.x += v * wv.x;
+            s.y += v * wv.y;
         }
-        a.h[((size_t)m * a.hps + (size_t)(leaf0 + lb) * a.nb + b) * R2 + r2] = s;
+        a.h[((size_t)m * a.hps + (size_t)(leaf0 + lb) * a.nb + b) * R2 + r2] = make_double2(sgn * s.x, sgn * s.y);
     }
 }
 
@@ -273,10 +277,12 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
         }
     }
     if (a.CS > 1) {
+        if (cs < a.CS) {
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
+            for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-            for (int r = 0; r < R2; ++r) red[((size_t)cs * a.RB + rl) * (NB * R2) + nb * R2 + r] = acc[nb][r];
+                for (int r = 0; r < R2; ++r) red[((size_t)cs * a.RB + rl) * (NB * R2) + nb * R2 + r] = acc[nb][r];
+        }
         __syncthreads();
         if (cs == 0) {
             for (int s = 1; s < a.CS; ++s)
@@ -847,8 +853,8 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
     const int thr = ((q2 + 31) / 32) * 32;
     {
         LeafUpArgs a{};
-        a.Ainv = d_Ainv; a.F = d_F; a.cF = d_cF; a.NI = d_NI; a.w = d_w; a.h = d_h[0]; a.hps = hstride;
-        a.q2 = q2; a.nb = nb; a.nF = nF; a.nelem = nelem; a.shared = shared ? 1 : 0;
+        a.Ainv = d_Ainv; a.F = d_F; a.cF = d_cF; a.D = d_D; a.c1 = c1; a.w = d_w; a.h = d_h[0]; a.hps = hstride;
+        a.q = q; a.q2 = q2; a.nb = nb; a.nF = nF; a.nelem = nelem; a.shared = shared ? 1 : 0;
         dim3 grid(nelem / NBl, nh);
         const size_t smem = static_cast<size_t>(NBl) * q2 * R2 * sizeof(double2);
         tbeg(s);
