@@ -208,8 +208,8 @@ def run_ours(args, cfg):
                         device=-1, half_range=(0, 1), nrhs=cfg["nrhs"])
         nh_total = tmp.num_half_poles
         tmp.close()
-        lo = nh_total * rank // world
-        hi = nh_total * (rank + 1) // world
+        from paper_1402_5168_b200.parallel import half_range
+        lo, hi = half_range(nh_total, rank, world)
         h = api.setup(cfg["model"], cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"],
                       device=local, half_range=(lo, hi), nrhs=cfg["nrhs"])
     else:
