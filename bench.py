@@ -96,43 +96,88 @@ def make_problem(cfg, x, y):
     return kappa
 
 
+def tree_dims(n, q):
+    """(nodes, n3, next) of every merge level (x-merge first, alternating), as in mesh.cpp."""
+    out = []
+    ac = bc = 1
+    lev = 0
+    while not (ac == n and bc == n):
+        if lev % 2 == 0:
+            a, b, n3 = 2 * ac, bc, bc * q
+        else:
+            a, b, n3 = ac, 2 * bc, ac * q
+        out.append(((n // a) * (n // b), n3, 2 * (a + b) * q))
+        ac, bc = a, b
+        lev += 1
+    return out
+
+
+def class_work(cfg, nh, R2, shared):
+    """Algorithmic FP64 flops and operator bytes per step, per kernel class.
+    Complex multiply-add = 8 flops; operator element = 16 bytes."""
+    n, q = cfg["n"], cfg["p"] - 2
+    q2, e = q * q, n * n
+    lv = tree_dims(n, q)
+    per = lambda nodes: 1 if shared else nodes
+    w = {
+        "leaf_up": (nh * e * q2 * q2 * R2 * 8, nh * per(e) * q2 * q2 * 16),
+        "leaf_flux": (nh * e * 4 * q * q * R2 * 4, 0),
+        "merge_up": (sum(nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx in lv),
+                     sum(nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx in lv)),
+        "root": (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16),
+        "merge_down": (sum(nh * nd * n3 * nx * R2 * 8 for nd, n3, nx in lv),
+                       sum(nh * per(nd) * n3 * nx * 16 for nd, n3, nx in lv)),
+        "leaf_down": (nh * e * q2 * 4 * q * R2 * 8, nh * per(e) * q2 * 4 * q * 16),
+    }
+    return w
+
+
 def roofline_for(cfg, h, times, steps, pk):
-    """Dominant kernel = the class with the largest device time.  Algorithmic work
-    per launch from DESIGN.md §6 (flops of the dense complex mat-vecs, or bytes
-    of the operators they stream)."""
-    q = cfg["p"] - 2
-    q2 = q * q
-    nelem = cfg["n"] ** 2
+    """Dominant kernel = the class with the largest device time.  achieved =
+    algorithmic work per launch / average launch time (CUDA events on the
+    launching stream)."""
     nh = h.num_half_poles
     R2 = 2 * h.nrhs
     shared = (cfg["model"] == "rsw")
+    work = class_work(cfg, nh, R2, shared)
     dom = max(times, key=lambda k: times[k][0])
     ms, nl = times[dom]
     per_launch_ms = ms / max(nl, 1)
     sm_max = pk.get("sm_max_mhz", 1965.0)
-    fp64_peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12      # TFLOP/s, FP64 FMA pipe at max clock
-    if dom == "leaf_up":
-        flops = nh * nelem * (q2 * q2 * R2 * 8 + 4 * q * q * R2 * 4)
-        bytes_ = nh * (1 if shared else nelem) * q2 * q2 * 16
-    elif dom == "leaf_down":
-        flops = nh * nelem * q2 * 4 * q * R2 * 8
-        bytes_ = nh * (1 if shared else nelem) * q2 * 4 * q * 16
-    else:
-        flops, bytes_ = None, None
-    if flops is None:
+    fp64_peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12      # 37.2 TFLOP/s; measured DMMA 37.2 (profiles/r01_fp64_peak.txt)
+    per_class = {}
+    for k, (t, c) in times.items():
+        if k in work and c:
+            fl, by = work[k]
+            launches_per_step = c / steps
+            sec = t / c * 1e-3
+            per_class[k] = {"tflops": round(fl / launches_per_step / sec / 1e12, 3),
+                            "operator_GBps": round(by / launches_per_step / sec / 1e9, 1)}
+    if dom not in work:
         return {"kernel": dom, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
-                "traffic": None}
+                "traffic": None, "per_class": per_class}
+    fl, by = work[dom]
+    lps = nl / steps
     if shared:
-        ach = flops / (per_launch_ms * 1e-3) / 1e12
+        ach = fl / lps / (per_launch_ms * 1e-3) / 1e12
         return {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(fp64_peak, 2),
-                "unit": "TFLOP/s", "frac": round(ach / fp64_peak, 4), "traffic": None,
-                "peak_source": "FP64 FMA pipe: 148 SMs x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md §6)",
-                "per_launch_ms": round(per_launch_ms, 4)}
+                "unit": "TFLOP/s", "frac": round(ach / fp64_peak, 4), "traffic": traffic_for(dom),
+                "peak_source": "FP64 pipe 148 SMs x 64 FMA/clk x 2 x sm_max_mhz = 37.2 TF; measured DMMA 37.2 TF",
+                "per_launch_ms": round(per_launch_ms, 4), "per_class": per_class}
     hbm = pk.get("hbm_gbs", 6650.0)
-    ach = bytes_ / (per_launch_ms * 1e-3) / 1e9
+    ach = by / lps / (per_launch_ms * 1e-3) / 1e9
     return {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(ach / hbm, 4), "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-            "per_launch_ms": round(per_launch_ms, 4)}
+            "frac": round(ach / hbm, 4), "traffic": traffic_for(dom), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+            "per_launch_ms": round(per_launch_ms, 4), "per_class": per_class}
+
+
+def traffic_for(kernel):
+    """dram read+write bytes per launch from the committed ncu --set full capture, if any."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return d.get(kernel)
+    except Exception:
+        return None
 
 
 def oracle_sample(cfg, npoles_sample, seconds_budget=30.0):

@@ -162,9 +162,9 @@ int32_t rexp_launches_per_step(const rexp_handle* h);
  * Between rexp_timing_begin and rexp_timing_end every kernel launch of the
  * handle is bracketed by CUDA events on its launching stream; timing_end
  * synchronizes on the last event and returns, per kernel class
- *   0 pre, 1 leaf_up, 2 merge_up, 3 root, 4 merge_down, 5 leaf_down,
- *   6 pole_sum, 7 recover,
- * the summed device milliseconds ms[8] and launch counts launches[8]. */
+ *   0 pre, 1 leaf_up, 2 leaf_flux, 3 merge_up, 4 root, 5 merge_down,
+ *   6 leaf_down, 7 pole_sum, 8 recover,
+ * the summed device milliseconds ms[9] and launch counts launches[9]. */
 int rexp_timing_begin(rexp_handle* h);
 int rexp_timing_end(rexp_handle* h, double* ms, int32_t* launches);
 

@@ -149,7 +149,7 @@ def step_finish(handle: Handle, e, u, stream=None):
                                             ctypes.c_void_p(_stream_ptr(stream))), "rexp_step_finish")
 
 
-KERNEL_CLASSES = ["pre", "leaf_up", "merge_up", "root", "merge_down", "leaf_down", "pole_sum", "recover"]
+KERNEL_CLASSES = ["pre", "leaf_up", "leaf_flux", "merge_up", "root", "merge_down", "leaf_down", "pole_sum", "recover"]
 
 
 def timing_begin(handle: Handle):
@@ -158,8 +158,8 @@ def timing_begin(handle: Handle):
 
 def timing_end(handle: Handle):
     """{class: (device_ms, launches)} accumulated since timing_begin (CUDA events)."""
-    ms = np.zeros(8)
-    cnt = np.zeros(8, dtype=np.int32)
+    ms = np.zeros(len(KERNEL_CLASSES))
+    cnt = np.zeros(len(KERNEL_CLASSES), dtype=np.int32)
     _lib.check(_lib.load().rexp_timing_end(handle.ptr, _dptr(ms), cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))),
                "rexp_timing_end")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}

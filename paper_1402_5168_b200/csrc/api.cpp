@@ -255,7 +255,9 @@ int64_t rexp_store_bytes(const rexp_handle* h) {
 }
 int64_t rexp_work_bytes(const rexp_handle* h) { return (h && h->dev) ? h->dev->work_bytes : 0; }
 int32_t rexp_launches_per_step(const rexp_handle* h) {
-    return h ? 6 + 3 * static_cast<int32_t>(h->T.levels.size()) : -1;
+    if (!h) return -1;
+    if (h->dev) return h->dev->launches_per_step();
+    return 6 + 3 * static_cast<int32_t>(h->T.levels.size());
 }
 
 

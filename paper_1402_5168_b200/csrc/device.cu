@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "rexp_device.hpp"
+#include "cgemm.cuh"
 
 namespace rexp {
 namespace dev {
@@ -185,6 +186,44 @@ __global__ void __launch_bounds__(256) k_leaf_up(LeafUpArgs a) {
         }
         a.h[((size_t)m * a.hps + (size_t)(leaf0 + lb) * a.nb + b) * R2 + r2] = make_double2(sgn * s.x, sgn * s.y);
     }
+}
+
+// --------------------------------------------------------------------------
+// k_leaf_flux: h = N_I w for every (half pole, leaf, boundary node, part) -
+// the outward normal derivative of the leaf particular solution (used when the
+// leaf solve ran as a GEMM that splits the leaf's rows over CTAs).
+// --------------------------------------------------------------------------
+struct FluxArgs {
+    const double2* w;       // [nh][nelem][q2][R2]
+    double2* h;             // [nh][hps][R2]
+    const double* D;
+    double c1;
+    long long hps;
+    int q, nelem, R2;
+};
+
+__global__ void k_leaf_flux(FluxArgs a) {
+    const int m = blockIdx.y;
+    const int nb = 4 * a.q, q = a.q, p = q + 2, q2 = q * q;
+    const long long per_pole = (long long)a.nelem * nb * a.R2;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= per_pole) return;
+    const int r2 = (int)(t % a.R2);
+    const int b = (int)((t / a.R2) % nb);
+    const int leaf = (int)(t / ((long long)a.R2 * nb));
+    const int side = b / q, s1 = b % q;
+    const double* drow = a.D + (side == 0 || side == 3 ? 0 : (p - 1) * p);
+    const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
+    const double2* wl = a.w + (((size_t)m * a.nelem + leaf) * q2) * a.R2 + r2;
+    double sx = 0.0, sy = 0.0;
+    for (int k = 1; k <= q; ++k) {
+        const int idx = (side == 0 || side == 2) ? (k - 1) * q + s1 : s1 * q + (k - 1);
+        const double v = __ldg(drow + k);
+        const double2 wv = wl[(size_t)idx * a.R2];
+        sx = fma(v, wv.x, sx);
+        sy = fma(v, wv.y, sy);
+    }
+    a.h[((size_t)m * a.hps + (size_t)leaf * nb + b) * a.R2 + r2] = make_double2(sgn * sx, sgn * sy);
 }
 
 // --------------------------------------------------------------------------
@@ -817,15 +856,70 @@ size_t gemv_smem(const GemvArgs& g, int NB, int R2) {
            sizeof(double2);
 }
 
+
+template <int MT, int WN, int R2, int MODE>
+void cg_launch(dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    k_cgemm<MT, WN, R2, MODE><<<grid, 32 * WN, cgemm_smem_bytes<MT, WN>(), s>>>(a);
+}
+template <int R2, int MODE>
+void cg_dispatch(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    if (WN == 8) {
+        switch (MT) {
+            case 2: cg_launch<2, 8, R2, MODE>(grid, s, a); break;
+            case 4: cg_launch<4, 8, R2, MODE>(grid, s, a); break;
+            default: cg_launch<5, 8, R2, MODE>(grid, s, a); break;
+        }
+    } else {
+        switch (MT) {
+            case 2: cg_launch<2, 4, R2, MODE>(grid, s, a); break;
+            case 4: cg_launch<4, 4, R2, MODE>(grid, s, a); break;
+            default: cg_launch<5, 4, R2, MODE>(grid, s, a); break;
+        }
+    }
+}
+template <int MODE>
+void cg_run(int R2, int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    if (R2 == 2) cg_dispatch<2, MODE>(MT, WN, grid, s, a);
+    else cg_dispatch<4, MODE>(MT, WN, grid, s, a);
+}
+template <int MT, int WN, int R2>
+void cg_allow_one() {
+    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_LEAF_UP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_LEAF_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_UPX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_UPY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+template <int R2>
+void cg_allow_r2() {
+    cg_allow_one<2, 8, R2>(); cg_allow_one<4, 8, R2>(); cg_allow_one<5, 8, R2>();
+    cg_allow_one<2, 4, R2>(); cg_allow_one<4, 4, R2>(); cg_allow_one<5, 4, R2>();
+}
+
+// tile choice for a GEMM with `rows` output rows and `ncols` columns:
+// fewest padded rows, ties to the larger tile
+void cg_tile(int rows, int ncols, int& MT, int& WN) {
+    int best = 5, bestw = 1 << 30;
+    for (int mt : {5, 4, 2}) {
+        const int bm = 8 * mt;
+        const int waste = ((rows + bm - 1) / bm) * bm - rows;
+        if (waste < bestw) { best = mt; bestw = waste; }
+    }
+    MT = best;
+    WN = ncols >= 64 ? 8 : 4;
+}
+
 }  // namespace
 
 void DeviceStore::configure_kernels() {
+    cg_allow_r2<2>();
+    cg_allow_r2<4>();
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
 }
 
-int DeviceStore::launches_per_step() const { return 6 + 3 * static_cast<int>(levels.size()); }
+int DeviceStore::launches_per_step() const { return (shared && R2 <= 4 ? 7 : 6) + 3 * static_cast<int>(levels.size()); }
 
 int DeviceStore::check(const char* what) {
     const cudaError_t e = cudaGetLastError();
@@ -848,10 +942,28 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         k_pre<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
         tend(T_PRE, s);
     }
-    // leaves up
+    // GEMM path: shared store, nrhs <= 2 (DMMA complex GEMM over all nodes of a level)
+    const bool gemm = shared && R2 <= 4;
     const int NBl = pick_nb(nelem, R2, shared);
     const int thr = ((q2 + 31) / 32) * 32;
-    {
+    if (gemm) {
+        CgemmArgs a{};
+        a.A = d_Ainv; a.rows = q2; a.K = q2; a.nodes = nelem;
+        a.F = d_F; a.cF = d_cF; a.nF = nF; a.q2 = q2; a.dst = d_w;
+        int MT, WN;
+        cg_tile(q2, nelem * R2, MT, WN);
+        a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
+        const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
+        tbeg(s);
+        cg_run<CG_LEAF_UP>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+        tend(T_LEAF_UP, s);
+        FluxArgs fa{};
+        fa.w = d_w; fa.h = d_h[0]; fa.D = d_D; fa.c1 = c1; fa.hps = hstride; fa.q = q; fa.nelem = nelem; fa.R2 = R2;
+        const long long per_pole = static_cast<long long>(nelem) * nb * R2;
+        tbeg(s);
+        k_leaf_flux<<<dim3(static_cast<unsigned>((per_pole + 255) / 256), nh), 256, 0, s>>>(fa);
+        tend(T_LEAF_FLUX, s);
+    } else {
         LeafUpArgs a{};
         a.Ainv = d_Ainv; a.F = d_F; a.cF = d_cF; a.D = d_D; a.c1 = c1; a.w = d_w; a.h = d_h[0]; a.hps = hstride;
         a.q = q; a.q2 = q2; a.nb = nb; a.nF = nF; a.nelem = nelem; a.shared = shared ? 1 : 0;
@@ -865,12 +977,40 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         }
         tend(T_LEAF_UP, s);
     }
-    // NOTE: h per pole is stored with stride hstride (elements of R2-vectors)
     // merges up
     for (size_t li = 0; li < levels.size(); ++li) {
         Level& L = levels[li];
         const double2* hc = d_h[li % 2];
         double2* hp = d_h[(li + 1) % 2];
+        const bool lg = gemm && L.nodes * R2 >= 32;
+        if (lg) {
+            int MT, WN;
+            {  // X stage: w3 = Xneg (h^a_3 + h^b_3)
+                CgemmArgs a{};
+                a.A = L.X; a.rows = L.n3; a.K = L.n3; a.nodes = L.nodes;
+                a.src = hc; a.src_ps = hstride; a.bi0 = L.ia3; a.bi1 = L.ib3;
+                a.dst = L.w3; a.dst_ps = static_cast<long long>(L.nodes) * L.n3;
+                cg_tile(L.n3, L.nodes * R2, MT, WN);
+                a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
+                const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
+                tbeg(s);
+                cg_run<CG_UPX>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+                tend(T_MERGE_UP, s);
+            }
+            {  // Y stage: h = h_child[ext] + Y w3
+                CgemmArgs a{};
+                a.A = L.Y; a.rows = L.next; a.K = L.n3; a.nodes = L.nodes;
+                a.src = L.w3; a.src_ps = static_cast<long long>(L.nodes) * L.n3;
+                a.dst = hp; a.dst_ps = hstride; a.add = hc; a.add_ps = hstride; a.ai0 = L.ext;
+                cg_tile(L.next, L.nodes * R2, MT, WN);
+                a.nrowblk = (L.next + 8 * MT - 1) / (8 * MT);
+                const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
+                tbeg(s);
+                cg_run<CG_UPY>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+                tend(T_MERGE_UP, s);
+            }
+            continue;
+        }
         const int NB = pick_nb(L.nodes, R2, shared);
         {  // X stage
             GemvArgs g = gemv_shape(L.n3, L.n3, L.nodes, shared);
@@ -907,6 +1047,21 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
     // merges down
     for (int li = static_cast<int>(levels.size()) - 1; li >= 0; --li) {
         Level& L = levels[li];
+        if (gemm && L.nodes * R2 >= 32) {
+            CgemmArgs a{};
+            a.A = L.S; a.rows = L.n3; a.K = L.next; a.nodes = L.nodes;
+            a.src = d_edge; a.src_ps = NE; a.bi0 = L.gext;
+            a.add = L.w3; a.add_ps = static_cast<long long>(L.nodes) * L.n3;
+            a.dst = d_edge; a.dst_ps = NE; a.so0 = L.g3;
+            int MT, WN;
+            cg_tile(L.n3, L.nodes * R2, MT, WN);
+            a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
+            const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
+            tbeg(s);
+            cg_run<CG_DOWN>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+            tend(T_MERGE_DOWN, s);
+            continue;
+        }
         const int NB = pick_nb(L.nodes, R2, shared);
         GemvArgs g = gemv_shape(L.n3, L.next, L.nodes, shared);
         g.M = L.S; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
@@ -918,7 +1073,18 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         tend(T_MERGE_DOWN, s);
     }
     // leaves down
-    {
+    if (gemm) {
+        CgemmArgs a{};
+        a.A = d_Sleaf; a.rows = q2; a.K = nb; a.nodes = nelem;
+        a.src = d_edge; a.src_ps = NE; a.bi0 = d_leaf_gB; a.dst = d_w;
+        int MT, WN;
+        cg_tile(q2, nelem * R2, MT, WN);
+        a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
+        const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
+        tbeg(s);
+        cg_run<CG_LEAF_DOWN>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+        tend(T_LEAF_DOWN, s);
+    } else {
         LeafDownArgs a{};
         a.S = d_Sleaf; a.edge = d_edge; a.gB = d_leaf_gB; a.w = d_w; a.NE = NE;
         a.q2 = q2; a.nb = nb; a.nelem = nelem; a.shared = shared ? 1 : 0;

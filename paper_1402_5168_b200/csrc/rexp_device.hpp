@@ -31,7 +31,7 @@ class DeviceStore {
     int launches_per_step() const;
 
     // per-kernel-class CUDA-event timing on the launching stream
-    enum { T_PRE = 0, T_LEAF_UP, T_MERGE_UP, T_ROOT, T_MERGE_DOWN, T_LEAF_DOWN, T_POLE_SUM, T_RECOVER, T_NCLASS };
+    enum { T_PRE = 0, T_LEAF_UP, T_LEAF_FLUX, T_MERGE_UP, T_ROOT, T_MERGE_DOWN, T_LEAF_DOWN, T_POLE_SUM, T_RECOVER, T_NCLASS };
     int timing_begin();
     int timing_end(double* ms, int32_t* launches);
 
