@@ -112,13 +112,26 @@ def tree_dims(n, q):
     return out
 
 
-def class_work(cfg, nh, R2, shared):
+def class_work(cfg, nh, R2, shared, leaf="dense"):
     """Algorithmic FP64 flops and operator bytes per step, per kernel class.
-    Complex multiply-add = 8 flops; operator element = 16 bytes."""
+    Complex multiply-add = 8 flops; operator element = 16 bytes.  leaf = "tensor":
+    four q x q x q real-by-complex products per leaf solve (16 q^3 flops), plus the
+    flux (UP) or the boundary lift (DOWN)."""
     n, q = cfg["n"], cfg["p"] - 2
     q2, e = q * q, n * n
     lv = tree_dims(n, q)
     per = lambda nodes: 1 if shared else nodes
+    if leaf == "tensor":
+        tensor_fl = nh * e * R2 * (16 * q ** 3)
+        return {
+            "leaf_up": (tensor_fl + nh * e * R2 * 4 * q * q * 4, nh * q * q * 16),
+            "leaf_down": (tensor_fl + nh * e * R2 * q2 * 4 * 2, nh * q * q * 16),
+            "merge_up": (sum(nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx in lv),
+                         sum(nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx in lv)),
+            "root": (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16),
+            "merge_down": (sum(nh * nd * n3 * nx * R2 * 8 for nd, n3, nx in lv),
+                           sum(nh * per(nd) * n3 * nx * 16 for nd, n3, nx in lv)),
+        }
     w = {
         "leaf_up": (nh * e * q2 * q2 * R2 * 8, nh * per(e) * q2 * q2 * 16),
         "leaf_flux": (nh * e * 4 * q * q * R2 * 4, 0),
@@ -139,7 +152,7 @@ def roofline_for(cfg, h, times, steps, pk):
     nh = h.num_half_poles
     R2 = 2 * h.nrhs
     shared = (cfg["model"] == "rsw")
-    work = class_work(cfg, nh, R2, shared)
+    work = class_work(cfg, nh, R2, shared, leaf=h.leaf_solver or "dense")
     dom = max(times, key=lambda k: times[k][0])
     ms, nl = times[dom]
     per_launch_ms = ms / max(nl, 1)
@@ -333,6 +346,7 @@ def run_ours(args, cfg):
                        "dof": dof, "nodes_per_field": N,
                        "baseline_nodes_per_field_convention": cfg["n"] ** 2 * cfg["p"] ** 2,
                        "store": "shared" if cfg["model"] == "rsw" else "pernode",
+                       "leaf_solver": h.leaf_solver,
                        "store_bytes": h.store_bytes, "work_bytes": h.work_bytes,
                        "l2": "operator store + work buffers exceed the 126 MB L2 (no flush needed)",
                        "parallelism": f"pole-sharded x{world}" if world > 1 else "single GPU"},

@@ -157,6 +157,9 @@ int64_t rexp_store_bytes(const rexp_handle* h);
 int64_t rexp_work_bytes(const rexp_handle* h);
 /* number of kernel launches one step issues (for the bench's gpu_launches) */
 int32_t rexp_launches_per_step(const rexp_handle* h);
+/* leaf solver of the device store: 0 = dense q^2 x q^2 leaf operators,
+ * 1 = tensor-product leaf inverse (constant coefficients), -1 = no device store */
+int32_t rexp_leaf_solver(const rexp_handle* h);
 
 /* ---- per-kernel timing (bench) ----
  * Between rexp_timing_begin and rexp_timing_end every kernel launch of the

@@ -66,6 +66,12 @@ class Handle:
         return int(_lib.load().rexp_launches_per_step(self.ptr))
 
     @property
+    def leaf_solver(self):
+        """'tensor' (tensor-product leaf inverse) or 'dense' (q^2 x q^2 leaf operators)."""
+        v = int(_lib.load().rexp_leaf_solver(self.ptr))
+        return {0: "dense", 1: "tensor"}.get(v, None)
+
+    @property
     def partial_len(self):
         return int(_lib.load().rexp_partial_len(self.ptr))
 

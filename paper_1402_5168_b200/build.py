@@ -15,7 +15,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU = ["device.cu"]
-CPP = ["rational.cpp", "mesh.cpp", "setup_host.cpp", "api.cpp"]
+CPP = ["rational.cpp", "mesh.cpp", "setup_host.cpp", "eig.cpp", "api.cpp"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

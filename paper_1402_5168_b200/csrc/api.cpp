@@ -261,6 +261,11 @@ int32_t rexp_launches_per_step(const rexp_handle* h) {
 }
 
 
+int32_t rexp_leaf_solver(const rexp_handle* h) {
+    if (!h || !h->dev) return -1;
+    return h->dev->fdm ? 1 : 0;
+}
+
 int rexp_timing_begin(rexp_handle* h) {
     int rc = need_device(h, false);
     if (rc) return rc;

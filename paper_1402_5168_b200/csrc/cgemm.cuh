@@ -41,7 +41,7 @@ struct CgemmArgs {
 };
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
@@ -53,29 +53,44 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// B gather in two phases so the global loads of chunk c+1 are in flight while
+// chunk c is multiplied: cg_fetch issues the loads into registers, cg_form
+// turns them into the B element (after the math).
+struct BRaw { double v[4]; };
+
 template <int R2, int MODE>
-__device__ __forceinline__ double2 cg_load_b(const CgemmArgs& a, int m, int k, int col) {
+__device__ __forceinline__ void cg_fetch(const CgemmArgs& a, int m, int k, int col, BRaw& r) {
     const int node = col / R2, r2 = col % R2;
     if (MODE == CG_LEAF_UP) {
         const double* f = a.F + ((size_t)(node * a.q2 + k) * a.nF) * R2 + r2;
-        const double2* c = a.cF + (size_t)m * a.nF;
-        double2 v = make_double2(0.0, 0.0);
-        for (int t = 0; t < a.nF; ++t) {
-            const double x = f[(size_t)t * R2];
-            const double2 ct = c[t];
-            v.x = fma(ct.x, x, v.x);
-            v.y = fma(ct.y, x, v.y);
-        }
-        return v;
+        r.v[0] = f[0];
+        r.v[1] = a.nF > 1 ? f[R2] : 0.0;
+        r.v[2] = a.nF > 2 ? f[2 * R2] : 0.0;
     } else if (MODE == CG_UPX) {
         const double2* s = a.src + (size_t)m * a.src_ps * R2;
         const double2 v0 = s[(size_t)a.bi0[(size_t)node * a.K + k] * R2 + r2];
         const double2 v1 = s[(size_t)a.bi1[(size_t)node * a.K + k] * R2 + r2];
-        return make_double2(v0.x + v1.x, v0.y + v1.y);
+        r.v[0] = v0.x; r.v[1] = v0.y; r.v[2] = v1.x; r.v[3] = v1.y;
     } else if (MODE == CG_UPY) {
-        return a.src[(size_t)m * a.src_ps * R2 + ((size_t)node * a.K + k) * R2 + r2];
+        const double2 v = a.src[(size_t)m * a.src_ps * R2 + ((size_t)node * a.K + k) * R2 + r2];
+        r.v[0] = v.x; r.v[1] = v.y;
     } else {  // LEAF_DOWN, DOWN: gather from the pole's edge array
-        return a.src[((size_t)m * a.src_ps + a.bi0[(size_t)node * a.K + k]) * R2 + r2];
+        const double2 v = a.src[((size_t)m * a.src_ps + a.bi0[(size_t)node * a.K + k]) * R2 + r2];
+        r.v[0] = v.x; r.v[1] = v.y;
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ double2 cg_form(const BRaw& r, const double2* cf) {
+    if (MODE == CG_LEAF_UP) {
+        double2 v;
+        v.x = fma(cf[0].x, r.v[0], fma(cf[1].x, r.v[1], cf[2].x * r.v[2]));
+        v.y = fma(cf[0].y, r.v[0], fma(cf[1].y, r.v[1], cf[2].y * r.v[2]));
+        return v;
+    } else if (MODE == CG_UPX) {
+        return make_double2(r.v[0] + r.v[2], r.v[1] + r.v[3]);
+    } else {
+        return make_double2(r.v[0], r.v[1]);
     }
 }
 
@@ -84,37 +99,32 @@ __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int
     const int node = col / R2, r2 = col % R2;
     if (MODE == CG_LEAF_UP) {
         a.dst[(((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2] = v;
-    } else if (MODE == CG_LEAF_DOWN) {
-        double2* p = a.dst + (((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2;
-        const double2 w = *p;
-        *p = make_double2(w.x + v.x, w.y + v.y);
+    } else if (MODE == CG_LEAF_DOWN) {   // additive w folded in by the caller
+        a.dst[(((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2] = v;
     } else if (MODE == CG_UPX) {
         a.dst[(size_t)m * a.dst_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2] = v;
     } else if (MODE == CG_UPY) {
         const double2 ad = a.add[((size_t)m * a.add_ps + a.ai0[(size_t)node * a.rows + row]) * R2 + r2];
         a.dst[(size_t)m * a.dst_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2] =
             make_double2(ad.x + v.x, ad.y + v.y);
-    } else {  // DOWN
-        const double2 ad = a.add[(size_t)m * a.add_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2];
-        a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * a.rows + row]) * R2 + r2] =
-            make_double2(ad.x + v.x, ad.y + v.y);
+    } else {  // DOWN (additive w3 folded in by the caller)
+        a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * a.rows + row]) * R2 + r2] = v;
     }
 }
 
-constexpr int CG_BK = 16;
-
-template <int MT, int WN>
+template <int MT, int WN, int BK, int NTW = 1>
 constexpr size_t cgemm_smem_bytes() {
-    return 2 * (size_t)CG_BK * ((8 * MT + 2) + (8 * WN + 2)) * sizeof(double2);
+    return 2 * (size_t)BK * ((8 * MT + 2) + (8 * WN * NTW + 2)) * sizeof(double2);
 }
 
-template <int MT, int WN, int R2, int MODE>
-__global__ void __launch_bounds__(32 * WN) k_cgemm(CgemmArgs a) {
-    constexpr int BM = 8 * MT, BN = 8 * WN, BK = CG_BK;
+// MT m-tiles and NTW n-tiles per warp; WN warps side by side in n.
+template <int MT, int WN, int BK, int R2, int MODE, int NTW = 1, int MINB = 1>
+__global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
+    constexpr int BM = 8 * MT, BN = 8 * WN * NTW, NT = 32 * WN;
+    static_assert(BK % 4 == 0, "BK must be a multiple of the DMMA k (4)");
     constexpr int LDA = BM + 2, LDB = BN + 2;
+    constexpr int BPT = (BK * BN + NT - 1) / NT;     // B elements per thread per chunk
     extern __shared__ double2 sm[];
-    double2* As[2] = {sm, sm + BK * LDA};
-    double2* Bs[2] = {sm + 2 * BK * LDA, sm + 2 * BK * LDA + BK * LDB};
 
     const int m = blockIdx.y;
     const int rb = blockIdx.x % a.nrowblk;
@@ -124,54 +134,123 @@ __global__ void __launch_bounds__(32 * WN) k_cgemm(CgemmArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     const double2* Am = a.A + (size_t)m * a.rows * a.K;
+    double2 cf[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+    if (MODE == CG_LEAF_UP) {
+        const double2* c = a.cF + (size_t)m * a.nF;
+        cf[0] = c[0];
+        if (a.nF > 1) cf[1] = c[1];
+        if (a.nF > 2) cf[2] = c[2];
+    }
 
-    auto load_chunk = [&](int buf, int k0) {
-        // A: BK columns x BM rows (column-major in global, contiguous rows)
-        for (int e = tid; e < BK * BM; e += 32 * WN) {
+    auto As = [&](int buf) { return sm + buf * BK * LDA; };
+    auto Bs = [&](int buf) { return sm + 2 * BK * LDA + buf * BK * LDB; };
+
+    auto issue_A = [&](int buf, int k0) {
+        double2* base = As(buf);
+        for (int e = tid; e < BK * BM; e += NT) {
             const int kk = e / BM, r = e % BM;
-            double2* dst = As[buf] + kk * LDA + r;
             const int row = row0 + r, k = k0 + kk;
-            if (row < a.rows && k < a.K) cp_async16(dst, Am + (size_t)k * a.rows + row);
-            else *dst = make_double2(0.0, 0.0);
-        }
-        // B: BK x BN, formed / gathered per mode
-        for (int e = tid; e < BK * BN; e += 32 * WN) {
-            const int kk = e / BN, c = e % BN;
-            const int k = k0 + kk, col = col0 + c;
-            double2 v = make_double2(0.0, 0.0);
-            if (k < a.K && col < ncols) v = cg_load_b<R2, MODE>(a, m, k, col);
-            Bs[buf][kk * LDB + c] = v;
+            if (row < a.rows && k < a.K) cp_async16(base + kk * LDA + r, Am + (size_t)k * a.rows + row);
+            else base[kk * LDA + r] = make_double2(0.0, 0.0);
         }
         cp_async_commit();
     };
-
-    double acc[MT][4];
+    BRaw braw[BPT];
+    auto fetch_B = [&](int k0) {
 #pragma unroll
-    for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+        for (int u = 0; u < BPT; ++u) {
+            const int e = tid + u * NT;
+            const int kk = e / BN, c = e % BN;
+            const int k = k0 + kk, col = col0 + c;
+            braw[u].v[0] = braw[u].v[1] = braw[u].v[2] = braw[u].v[3] = 0.0;
+            if (e < BK * BN && k < a.K && col < ncols) cg_fetch<R2, MODE>(a, m, k, col, braw[u]);
+        }
+    };
+    auto store_B = [&](int buf) {
+        double2* base = Bs(buf);
+#pragma unroll
+        for (int u = 0; u < BPT; ++u) {
+            const int e = tid + u * NT;
+            if (e < BK * BN) base[(e / BN) * LDB + (e % BN)] = cg_form<MODE>(braw[u], cf);
+        }
+    };
+
+    double acc[MT][NTW][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int n = 0; n < NTW; ++n) acc[i][n][0] = acc[i][n][1] = acc[i][n][2] = acc[i][n][3] = 0.0;
+
+    // additive epilogue terms (LEAF_DOWN: w, DOWN: w3) fetched before the K loop
+    constexpr bool kAdd = (MODE == CG_LEAF_DOWN || MODE == CG_DOWN);
+    double2 addv[kAdd ? MT : 1][kAdd ? NTW : 1][2];
+    if (kAdd) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int row = row0 + i * 8 + g;
+                    const int col = col0 + (warp * NTW + n) * 8 + 2 * t4 + j;
+                    addv[i][n][j] = make_double2(0.0, 0.0);
+                    if (row < a.rows && col < ncols) {
+                        const int node = col / R2, r2 = col % R2;
+                        if (MODE == CG_LEAF_DOWN)
+                            addv[i][n][j] = a.dst[(((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2];
+                        else
+                            addv[i][n][j] = a.add[(size_t)m * a.add_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2];
+                    }
+                }
+    }
 
     const int nchunks = (a.K + BK - 1) / BK;
-    load_chunk(0, 0);
+    issue_A(0, 0);
+    fetch_B(0);
+    store_B(0);
+    cp_async_wait_all();
+    __syncthreads();
     for (int ch = 0; ch < nchunks; ++ch) {
         const int buf = ch & 1;
-        cp_async_wait_all();
-        __syncthreads();
-        if (ch + 1 < nchunks) load_chunk(buf ^ 1, (ch + 1) * BK);
-        const double2* Ab = As[buf];
-        const double2* Bb = Bs[buf];
+        const bool more = ch + 1 < nchunks;
+        if (more) {
+            issue_A(buf ^ 1, (ch + 1) * BK);
+            fetch_B((ch + 1) * BK);
+        }
+        const double2* Ab = As(buf);
+        const double2* Bb = Bs(buf);
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
             const int kk = ks * 4 + t4;
-            const double2 b = Bb[kk * LDB + warp * 8 + g];   // B[k = t4][n = g]
-            const double nbi = -b.y;
+            double2 b[NTW];
 #pragma unroll
-            for (int i = 0; i < MT; ++i) {
-                const double2 av = Ab[kk * LDA + i * 8 + g];  // A[m = g][k = t4]
-                dmma884(acc[i][0], acc[i][1], av.x, b.x);    // Cr += Ar Br
-                dmma884(acc[i][0], acc[i][1], av.y, nbi);    // Cr += Ai (-Bi)
-                dmma884(acc[i][2], acc[i][3], av.x, b.y);    // Ci += Ar Bi
-                dmma884(acc[i][2], acc[i][3], av.y, b.x);    // Ci += Ai Br
-            }
+            for (int n = 0; n < NTW; ++n) b[n] = Bb[kk * LDB + (warp * NTW + n) * 8 + g];   // B[k = t4][n = g]
+            double2 av[MT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + i * 8 + g];   // A[m = g][k = t4]
+            // four passes so each accumulator is revisited only every 2*MT*NTW DMMAs
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[i][n][0], acc[i][n][1], av[i].x, b[n].x);    // Cr += Ar Br
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[i][n][2], acc[i][n][3], av[i].x, b[n].y);    // Ci += Ar Bi
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[i][n][0], acc[i][n][1], av[i].y, -b[n].y);   // Cr += Ai (-Bi)
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[i][n][2], acc[i][n][3], av[i].y, b[n].x);    // Ci += Ai Br
         }
+        if (more) {
+            store_B(buf ^ 1);
+            cp_async_wait_all();
+        }
+        __syncthreads();
     }
     // epilogue: C[g][2 t4 + j] of each tile
 #pragma unroll
@@ -179,10 +258,18 @@ __global__ void __launch_bounds__(32 * WN) k_cgemm(CgemmArgs a) {
         const int row = row0 + i * 8 + g;
         if (row >= a.rows) continue;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int col = col0 + warp * 8 + 2 * t4 + j;
-            if (col < ncols) cg_store<R2, MODE>(a, m, row, col, make_double2(acc[i][j], acc[i][2 + j]));
-        }
+        for (int n = 0; n < NTW; ++n)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int col = col0 + (warp * NTW + n) * 8 + 2 * t4 + j;
+                if (col >= ncols) continue;
+                double2 v = make_double2(acc[i][n][j], acc[i][n][2 + j]);
+                if (kAdd) {
+                    v.x += addv[i][n][j].x;
+                    v.y += addv[i][n][j].y;
+                }
+                cg_store<R2, MODE>(a, m, row, col, v);
+            }
     }
 }
 

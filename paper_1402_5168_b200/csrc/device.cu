@@ -18,12 +18,14 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
 
 #include "rexp_device.hpp"
 #include "cgemm.cuh"
+#include "leaf_fdm.cuh"
 
 namespace rexp {
 namespace dev {
@@ -202,28 +204,45 @@ struct FluxArgs {
     int q, nelem, R2;
 };
 
-__global__ void k_leaf_flux(FluxArgs a) {
+// one CTA per (half pole, group of FLUX_LB leaves): stage w coalesced, then
+// each thread forms one (leaf, boundary node, part) line sum
+constexpr int FLUX_LB = 8;
+__global__ void __launch_bounds__(256) k_leaf_flux(FluxArgs a) {
+    extern __shared__ double2 ws[];                 // [FLUX_LB][q2][R2]
     const int m = blockIdx.y;
-    const int nb = 4 * a.q, q = a.q, p = q + 2, q2 = q * q;
-    const long long per_pole = (long long)a.nelem * nb * a.R2;
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= per_pole) return;
-    const int r2 = (int)(t % a.R2);
-    const int b = (int)((t / a.R2) % nb);
-    const int leaf = (int)(t / ((long long)a.R2 * nb));
-    const int side = b / q, s1 = b % q;
-    const double* drow = a.D + (side == 0 || side == 3 ? 0 : (p - 1) * p);
-    const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
-    const double2* wl = a.w + (((size_t)m * a.nelem + leaf) * q2) * a.R2 + r2;
-    double sx = 0.0, sy = 0.0;
-    for (int k = 1; k <= q; ++k) {
-        const int idx = (side == 0 || side == 2) ? (k - 1) * q + s1 : s1 * q + (k - 1);
-        const double v = __ldg(drow + k);
-        const double2 wv = wl[(size_t)idx * a.R2];
-        sx = fma(v, wv.x, sx);
-        sy = fma(v, wv.y, sy);
+    const int leaf0 = blockIdx.x * FLUX_LB;
+    const int q = a.q, p = q + 2, q2 = q * q, nb = 4 * q, R2 = a.R2;
+    const int nl = min(FLUX_LB, a.nelem - leaf0);
+    const double2* src = a.w + (((size_t)m * a.nelem + leaf0) * q2) * R2;
+    const int tot = nl * q2 * R2;
+    int t0 = threadIdx.x;
+    for (; t0 + 3 * (int)blockDim.x < tot; t0 += 4 * blockDim.x) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = src[t0 + u * blockDim.x];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ws[t0 + u * blockDim.x] = v[u];
     }
-    a.h[((size_t)m * a.hps + (size_t)leaf * nb + b) * a.R2 + r2] = make_double2(sgn * sx, sgn * sy);
+    for (; t0 < tot; t0 += blockDim.x) ws[t0] = src[t0];
+    __syncthreads();
+    for (int t = threadIdx.x; t < nl * nb * R2; t += blockDim.x) {
+        const int r2 = t % R2;
+        const int b = (t / R2) % nb;
+        const int lb = t / (R2 * nb);
+        const int side = b / q, s1 = b % q;
+        const double* drow = a.D + (side == 0 || side == 3 ? 0 : (p - 1) * p);
+        const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
+        const double2* wl = ws + (size_t)lb * q2 * R2 + r2;
+        double sx = 0.0, sy = 0.0;
+        for (int k = 1; k <= q; ++k) {
+            const int idx = (side == 0 || side == 2) ? (k - 1) * q + s1 : s1 * q + (k - 1);
+            const double v = __ldg(drow + k);
+            const double2 wv = wl[(size_t)idx * R2];
+            sx = fma(v, wv.x, sx);
+            sy = fma(v, wv.y, sy);
+        }
+        a.h[((size_t)m * a.hps + (size_t)(leaf0 + lb) * nb + b) * R2 + r2] = make_double2(sgn * sx, sgn * sy);
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -296,12 +315,12 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
         const double2* M = a.M + mat + row;
         const int CS = a.CS;
         int c = cs;
-        for (; c + 3 * CS < cols; c += 4 * CS) {
-            double2 mv[4];
+        for (; c + 7 * CS < cols; c += 8 * CS) {
+            double2 mv[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) mv[u] = ldg2(M + (size_t)(c + u * CS) * rows);
+            for (int u = 0; u < 8; ++u) mv[u] = ldg2(M + (size_t)(c + u * CS) * rows);
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 8; ++u)
 #pragma unroll
                 for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
@@ -444,7 +463,25 @@ __global__ void k_pole_sum(PoleSumArgs a) {
     const bool inter = g < a.NI;
     const double2* base = inter ? (a.w + g * a.R2 + r2) : (a.edge + (g - a.NI) * a.R2 + r2);
     const long long ps = (inter ? a.NI : a.NE) * a.R2;
-    for (int m = 0; m < a.nh; ++m) {
+    // 4 poles' loads in flight; accumulation stays in ascending pole order
+    int m = 0;
+    for (; m + 4 <= a.nh; m += 4) {
+        double2 u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = base[(size_t)(m + k) * ps];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2* d = a.dE + (size_t)(m + k) * a.nE;
+            const double2 d0 = d[0], d1 = d[1];
+            s0 += d0.x * u[k].x - d0.y * u[k].y;
+            s1 += d1.x * u[k].x - d1.y * u[k].y;
+            if (a.nE > 2) {
+                const double2 d2 = d[2];
+                s2 += d2.x * u[k].x - d2.y * u[k].y;
+            }
+        }
+    }
+    for (; m < a.nh; ++m) {
         const double2 u = base[(size_t)m * ps];
         const double2* d = a.dE + (size_t)m * a.nE;
         const double2 d0 = d[0], d1 = d[1];
@@ -727,8 +764,43 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         store_bytes += static_cast<int64_t>(v.size()) * 16;
         return put(d, tmp);
     };
-    if ((rc = put_ops(ops[0].m[0], &d_Ainv))) return rc;
-    if ((rc = put_ops(ops[0].m[1], &d_Sleaf))) return rc;
+    // tensor-product leaf inverse for constant coefficients (RSW shared store),
+    // unless REXP_LEAF=dense asks for the dense q^2 x q^2 leaf operators
+    {
+        const char* env = std::getenv("REXP_LEAF");
+        const bool want_dense = env && std::string(env) == "dense";
+        fdm = shared && model == REXP_MODEL_RSW && q <= FDM_T && R2 <= 8 && !want_dense;
+    }
+    if ((rc = put(&d_D2, ch.D2))) return rc;
+    if (fdm) {
+        std::vector<double> K(static_cast<size_t>(q) * q), lam, V, Vi;
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j) K[static_cast<size_t>(i) * q + j] = ch.D2[(i + 1) * p + (j + 1)];
+        if ((rc = real_eig(q, K, lam, V, Vi))) return rc;
+        std::vector<double> Vp(FDM_T * FDM_T, 0.0), Vip(FDM_T * FDM_T, 0.0);
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j) {
+                Vp[i * FDM_T + j] = V[static_cast<size_t>(i) * q + j];
+                Vip[i * FDM_T + j] = Vi[static_cast<size_t>(i) * q + j];
+            }
+        const double c2 = c1 * c1;
+        std::vector<double2> Dinv(static_cast<size_t>(nh) * FDM_T * FDM_T, make_double2(0.0, 0.0));
+        for (int m = 0; m < nh; ++m) {
+            const cd sg = pt.shift[h0 + m];
+            for (int i = 0; i < q; ++i)
+                for (int j = 0; j < q; ++j) {
+                    const cd v = 1.0 / (c2 * (lam[i] + lam[j]) - sg);
+                    Dinv[(static_cast<size_t>(m) * FDM_T + i) * FDM_T + j] = make_double2(v.real(), v.imag());
+                }
+        }
+        if ((rc = put(&d_V, Vp))) return rc;
+        if ((rc = put(&d_Vinv, Vip))) return rc;
+        if ((rc = put(&d_Dinv, Dinv))) return rc;
+        store_bytes += static_cast<int64_t>(Dinv.size()) * 16;
+    } else {
+        if ((rc = put_ops(ops[0].m[0], &d_Ainv))) return rc;
+        if ((rc = put_ops(ops[0].m[1], &d_Sleaf))) return rc;
+    }
     if ((rc = put(&d_leaf_gB, T.leaf_gB))) return rc;
     levels.resize(T.levels.size());
     for (size_t li = 0; li < T.levels.size(); ++li) {
@@ -842,8 +914,10 @@ GemvArgs gemv_shape(int rows, int cols, int nodes, bool shared) {
     g.cols = cols;
     g.nodes = nodes;
     g.shared = shared ? 1 : 0;
+    // 64-row blocks split 4 ways over columns: many CTAs and >= 8 loads in
+    // flight per thread keep the HBM stream of the top (1-2 node) levels busy
     int rb = ((rows + 31) / 32) * 32;
-    if (rb > 256) rb = 256;
+    if (rb > 64) rb = 64;
     g.RB = rb;
     g.CS = 256 / rb;
     if (g.CS > 8) g.CS = 8;
@@ -857,44 +931,54 @@ size_t gemv_smem(const GemvArgs& g, int NB, int R2) {
 }
 
 
-template <int MT, int WN, int R2, int MODE>
+template <int MT, int WN, int BK, int R2, int MODE>
 void cg_launch(dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    k_cgemm<MT, WN, R2, MODE><<<grid, 32 * WN, cgemm_smem_bytes<MT, WN>(), s>>>(a);
+    k_cgemm<MT, WN, BK, R2, MODE><<<grid, 32 * WN, cgemm_smem_bytes<MT, WN, BK>(), s>>>(a);
 }
-template <int R2, int MODE>
-void cg_dispatch(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    if (WN == 8) {
-        switch (MT) {
-            case 2: cg_launch<2, 8, R2, MODE>(grid, s, a); break;
-            case 4: cg_launch<4, 8, R2, MODE>(grid, s, a); break;
-            default: cg_launch<5, 8, R2, MODE>(grid, s, a); break;
-        }
-    } else {
-        switch (MT) {
-            case 2: cg_launch<2, 4, R2, MODE>(grid, s, a); break;
-            case 4: cg_launch<4, 4, R2, MODE>(grid, s, a); break;
-            default: cg_launch<5, 4, R2, MODE>(grid, s, a); break;
-        }
+template <int WN, int BK, int R2, int MODE>
+void cg_mt(int MT, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    switch (MT) {
+        case 2: cg_launch<2, WN, BK, R2, MODE>(grid, s, a); break;
+        case 4: cg_launch<4, WN, BK, R2, MODE>(grid, s, a); break;
+        default: cg_launch<5, WN, BK, R2, MODE>(grid, s, a); break;
     }
 }
+template <int BK, int R2, int MODE>
+void cg_wn(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    switch (WN) {
+        case 1: cg_mt<1, BK, R2, MODE>(MT, grid, s, a); break;
+        case 2: cg_mt<2, BK, R2, MODE>(MT, grid, s, a); break;
+        case 4: cg_mt<4, BK, R2, MODE>(MT, grid, s, a); break;
+        default: cg_mt<8, BK, R2, MODE>(MT, grid, s, a); break;
+    }
+}
+// BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16
 template <int MODE>
-void cg_run(int R2, int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    if (R2 == 2) cg_dispatch<2, MODE>(MT, WN, grid, s, a);
-    else cg_dispatch<4, MODE>(MT, WN, grid, s, a);
+void cg_run(int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    const bool b28 = (K % 28) == 0;
+    if (R2 == 2) {
+        if (b28) cg_wn<28, 2, MODE>(MT, WN, grid, s, a);
+        else cg_wn<16, 2, MODE>(MT, WN, grid, s, a);
+    } else {
+        if (b28) cg_wn<28, 4, MODE>(MT, WN, grid, s, a);
+        else cg_wn<16, 4, MODE>(MT, WN, grid, s, a);
+    }
 }
-template <int MT, int WN, int R2>
+template <int MT, int WN, int BK, int R2>
 void cg_allow_one() {
-    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_LEAF_UP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_LEAF_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_UPX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_UPY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, R2, CG_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int lim = 200 * 1024;
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_LEAF_UP>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_LEAF_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_UPX>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_UPY>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
 }
+template <int WN, int BK, int R2>
+void cg_allow_mt() { cg_allow_one<2, WN, BK, R2>(); cg_allow_one<4, WN, BK, R2>(); cg_allow_one<5, WN, BK, R2>(); }
+template <int BK, int R2>
+void cg_allow_wn() { cg_allow_mt<1, BK, R2>(); cg_allow_mt<2, BK, R2>(); cg_allow_mt<4, BK, R2>(); cg_allow_mt<8, BK, R2>(); }
 template <int R2>
-void cg_allow_r2() {
-    cg_allow_one<2, 8, R2>(); cg_allow_one<4, 8, R2>(); cg_allow_one<5, 8, R2>();
-    cg_allow_one<2, 4, R2>(); cg_allow_one<4, 4, R2>(); cg_allow_one<5, 4, R2>();
-}
+void cg_allow_r2() { cg_allow_wn<16, R2>(); cg_allow_wn<28, R2>(); }
 
 // tile choice for a GEMM with `rows` output rows and `ncols` columns:
 // fewest padded rows, ties to the larger tile
@@ -906,12 +990,15 @@ void cg_tile(int rows, int ncols, int& MT, int& WN) {
         if (waste < bestw) { best = mt; bestw = waste; }
     }
     MT = best;
-    WN = ncols >= 64 ? 8 : 4;
+    WN = ncols >= 64 ? 8 : ncols >= 32 ? 4 : ncols >= 16 ? 2 : 1;
 }
 
 }  // namespace
 
 void DeviceStore::configure_kernels() {
+    cudaFuncSetAttribute(k_leaf_fdm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_fdm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cg_allow_r2<2>();
     cg_allow_r2<4>();
     allow_all<2>();
@@ -919,7 +1006,7 @@ void DeviceStore::configure_kernels() {
     allow_all<8>();
 }
 
-int DeviceStore::launches_per_step() const { return (shared && R2 <= 4 ? 7 : 6) + 3 * static_cast<int>(levels.size()); }
+int DeviceStore::launches_per_step() const { return (shared && R2 <= 4 && !fdm ? 7 : 6) + 3 * static_cast<int>(levels.size()); }
 
 int DeviceStore::check(const char* what) {
     const cudaError_t e = cudaGetLastError();
@@ -946,7 +1033,20 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
     const bool gemm = shared && R2 <= 4;
     const int NBl = pick_nb(nelem, R2, shared);
     const int thr = ((q2 + 31) / 32) * 32;
-    if (gemm) {
+    FdmArgs fd{};
+    if (fdm) {
+        fd.V = d_V; fd.Vinv = d_Vinv; fd.Dinv = d_Dinv; fd.D = d_D; fd.D2 = d_D2; fd.F = d_F; fd.cF = d_cF;
+        fd.q = q; fd.p = p; fd.nF = nF; fd.nelem = nelem; fd.R2 = R2; fd.nh = nh; fd.c1 = c1; fd.c2 = c1 * c1;
+        fd.h = d_h[0]; fd.hps = hstride; fd.edge = d_edge; fd.NE = NE; fd.gB = d_leaf_gB; fd.w = d_w;
+    }
+    const long long nprob = static_cast<long long>(nh) * nelem * R2;
+    const unsigned fdm_blocks = static_cast<unsigned>((nprob + FDM_WARPS - 1) / FDM_WARPS);
+    const size_t fdm_smem = static_cast<size_t>(FDM_WARPS) * FDM_TILE_ELEMS * sizeof(double2);
+    if (fdm) {
+        tbeg(s);
+        k_leaf_fdm<0><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
+        tend(T_LEAF_UP, s);
+    } else if (gemm) {
         CgemmArgs a{};
         a.A = d_Ainv; a.rows = q2; a.K = q2; a.nodes = nelem;
         a.F = d_F; a.cF = d_cF; a.nF = nF; a.q2 = q2; a.dst = d_w;
@@ -955,13 +1055,13 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
         const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
         tbeg(s);
-        cg_run<CG_LEAF_UP>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+        cg_run<CG_LEAF_UP>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
         tend(T_LEAF_UP, s);
         FluxArgs fa{};
         fa.w = d_w; fa.h = d_h[0]; fa.D = d_D; fa.c1 = c1; fa.hps = hstride; fa.q = q; fa.nelem = nelem; fa.R2 = R2;
-        const long long per_pole = static_cast<long long>(nelem) * nb * R2;
         tbeg(s);
-        k_leaf_flux<<<dim3(static_cast<unsigned>((per_pole + 255) / 256), nh), 256, 0, s>>>(fa);
+        k_leaf_flux<<<dim3((nelem + FLUX_LB - 1) / FLUX_LB, nh), 256,
+                      static_cast<size_t>(FLUX_LB) * q2 * R2 * sizeof(double2), s>>>(fa);
         tend(T_LEAF_FLUX, s);
     } else {
         LeafUpArgs a{};
@@ -982,7 +1082,7 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         Level& L = levels[li];
         const double2* hc = d_h[li % 2];
         double2* hp = d_h[(li + 1) % 2];
-        const bool lg = gemm && L.nodes * R2 >= 32;
+        const bool lg = gemm && L.nodes * R2 >= 4;
         if (lg) {
             int MT, WN;
             {  // X stage: w3 = Xneg (h^a_3 + h^b_3)
@@ -994,7 +1094,7 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
                 a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
                 const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
                 tbeg(s);
-                cg_run<CG_UPX>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+                cg_run<CG_UPX>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
                 tend(T_MERGE_UP, s);
             }
             {  // Y stage: h = h_child[ext] + Y w3
@@ -1006,7 +1106,7 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
                 a.nrowblk = (L.next + 8 * MT - 1) / (8 * MT);
                 const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
                 tbeg(s);
-                cg_run<CG_UPY>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+                cg_run<CG_UPY>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
                 tend(T_MERGE_UP, s);
             }
             continue;
@@ -1047,7 +1147,7 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
     // merges down
     for (int li = static_cast<int>(levels.size()) - 1; li >= 0; --li) {
         Level& L = levels[li];
-        if (gemm && L.nodes * R2 >= 32) {
+        if (gemm && L.nodes * R2 >= 4) {
             CgemmArgs a{};
             a.A = L.S; a.rows = L.n3; a.K = L.next; a.nodes = L.nodes;
             a.src = d_edge; a.src_ps = NE; a.bi0 = L.gext;
@@ -1058,7 +1158,7 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
             a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
             const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
             tbeg(s);
-            cg_run<CG_DOWN>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+            cg_run<CG_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
             tend(T_MERGE_DOWN, s);
             continue;
         }
@@ -1073,7 +1173,11 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         tend(T_MERGE_DOWN, s);
     }
     // leaves down
-    if (gemm) {
+    if (fdm) {
+        tbeg(s);
+        k_leaf_fdm<1><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
+        tend(T_LEAF_DOWN, s);
+    } else if (gemm) {
         CgemmArgs a{};
         a.A = d_Sleaf; a.rows = q2; a.K = nb; a.nodes = nelem;
         a.src = d_edge; a.src_ps = NE; a.bi0 = d_leaf_gB; a.dst = d_w;
@@ -1082,7 +1186,7 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
         const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
         tbeg(s);
-        cg_run<CG_LEAF_DOWN>(R2, MT, WN, dim3(a.nrowblk * ncb, nh), s, a);
+        cg_run<CG_LEAF_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
         tend(T_LEAF_DOWN, s);
     } else {
         LeafDownArgs a{};

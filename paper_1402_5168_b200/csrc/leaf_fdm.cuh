@@ -1,0 +1,223 @@
+// Tensor-product leaf solve for the constant-coefficient (shared) store.
+//
+// On a leaf the interior collocation operator is a Kronecker sum
+//     A_II = c2 (I (x) K + K (x) I) - sigma,   K = D2[1..q][1..q],  c2 = (2/H)^2
+// (§2.2 collocation; interior index (i, j), i fastest), so with
+// K = V diag(l) V^-1 (real, kappa(V) ~ 1.6 for q <= 16):
+//     A_II^{-1} F = V [ (V^-1 F V^-T) ./ (c2 (l_i + l_j) - sigma) ] V^T        (F: q x q)
+// which is exactly the leaf inverse of the HPS solver, applied with four
+// 16 x 16 (zero-padded) real x complex products on the FP64 tensor pipe
+// (DMMA m8n8k4) instead of one dense q^2 x q^2 complex mat-vec: 7x fewer flops.
+//
+// One warp owns one (half pole, leaf, real RHS part) problem; tiles live in
+// shared memory; only __syncwarp is needed.
+//   UP:   u = A_II^{-1} f;  h = N_I u (outward normal flux at the 4q boundary nodes)
+//   DOWN: u = A_II^{-1} (f - A_IB u_B) = interior solution (written for the pole sum)
+#pragma once
+
+namespace rexp {
+namespace dev {
+
+constexpr int FDM_T = 16;          // padded tile edge
+constexpr int FDM_LDT = 20;        // tile stride: conflict-free for transposed fragment reads
+constexpr int FDM_LDD = FDM_LDT;   // (the single direct read, stage 1, takes 2-way conflicts)
+constexpr int FDM_WARPS = 8;
+constexpr int FDM_TILE_ELEMS = 2 * FDM_T * FDM_LDT + 4 * 16;     // tiles X, Y + boundary values
+
+struct FdmArgs {
+    const double* V;        // 16 x 16 row-major, zero padded
+    const double* Vinv;     // 16 x 16 row-major, zero padded
+    const double2* Dinv;    // [nh][16*16] 1/(c2 (l_i + l_j) - sigma_m), zero padded
+    const double* D;        // p x p
+    const double* D2;       // p x p
+    const double* F;        // [NI][nF][R2]
+    const double2* cF;      // [nh][nF]
+    int q, p, nF, nelem, R2, nh;
+    double c1, c2;
+    // UP
+    double2* h;             // [nh][hps][R2]
+    long long hps;
+    // DOWN
+    const double2* edge;    // [nh][NE][R2]
+    long long NE;
+    const int* gB;          // [nelem][4q]
+    double2* w;             // [nh][nelem][q2][R2]
+};
+
+__device__ __forceinline__ void dmma884r(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+// C (16x16 complex, in fragments) = A (16x16 real, fragments af) * B, where
+// B[k][n] = TRANS ? X[n*LD + k] : X[k*LD + n]  (complex tile in shared memory).
+template <bool TRANS, int LD>
+__device__ __forceinline__ void fdm_stage(const double (&af)[2][4], const double2* X, int g, int t4,
+                                          double (&cr)[2][2][2], double (&ci)[2][2][2]) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) cr[mt][nt][0] = cr[mt][nt][1] = ci[mt][nt][0] = ci[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+        const int k = ks * 4 + t4;
+        double2 b[2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int n = nt * 8 + g;
+            b[nt] = TRANS ? X[n * LD + k] : X[k * LD + n];
+        }
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) dmma884r(cr[mt][nt][0], cr[mt][nt][1], af[mt][ks], b[nt].x);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) dmma884r(ci[mt][nt][0], ci[mt][nt][1], af[mt][ks], b[nt].y);
+    }
+}
+
+template <int MODE>   // 0 = UP, 1 = DOWN
+__global__ void __launch_bounds__(32 * FDM_WARPS) k_leaf_fdm(FdmArgs a) {
+    extern __shared__ double2 fsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const long long prob = (long long)blockIdx.x * FDM_WARPS + warp;
+    const long long nprob = (long long)a.nh * a.nelem * a.R2;
+    if (prob >= nprob) return;
+    const int r2 = (int)(prob % a.R2);
+    const int leaf = (int)((prob / a.R2) % a.nelem);
+    const int m = (int)(prob / ((long long)a.R2 * a.nelem));
+    const int q = a.q, p = a.p, q2 = q * q, nb = 4 * q;
+    double2* P = fsm + (size_t)warp * FDM_TILE_ELEMS;      // T, then S2^T (scaled), then U
+    double2* Q = P + FDM_T * FDM_LDT;                       // S1, then S3
+    double2* R = P;
+    double2* UB = Q + FDM_T * FDM_LDT;                      // boundary values (DOWN), 4q <= 64
+
+    // A fragments: af[mt][ks] = A[mt*8 + g][ks*4 + t4]
+    double vf[2][4], vif[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            vf[mt][ks] = __ldg(a.V + (mt * 8 + g) * FDM_T + ks * 4 + t4);
+            vif[mt][ks] = __ldg(a.Vinv + (mt * 8 + g) * FDM_T + ks * 4 + t4);
+        }
+
+    // ---- right-hand side T = f (UP) or f - A_IB u_B (DOWN), zero padded ----
+    const double2* cf = a.cF + (size_t)m * a.nF;
+    const double2 c0 = cf[0];
+    const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0, 0);
+    const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0, 0);
+    if (MODE == 1) {
+        for (int b = lane; b < nb; b += 32)
+            UB[b] = a.edge[((size_t)m * a.NE + a.gB[(size_t)leaf * nb + b]) * a.R2 + r2];
+        __syncwarp();
+    }
+    for (int e = lane; e < FDM_T * FDM_T; e += 32) {
+        const int i = e % FDM_T, j = e / FDM_T;
+        double2 v = make_double2(0.0, 0.0);
+        if (i < q && j < q) {
+            const double* f = a.F + ((size_t)((size_t)leaf * q2 + j * q + i) * a.nF) * a.R2 + r2;
+            const double f0 = f[0];
+            const double f1 = a.nF > 1 ? f[a.R2] : 0.0;
+            const double f2 = a.nF > 2 ? f[2 * a.R2] : 0.0;
+            v.x = c0.x * f0 + c1v.x * f1 + c2v.x * f2;
+            v.y = c0.y * f0 + c1v.y * f1 + c2v.y * f2;
+            if (MODE == 1) {
+                // A_IB u_B at interior (i+1, j+1): row i+1 meets left/right, column j+1 meets bottom/top
+                const double dl = a.D2[(i + 1) * p + 0], dr = a.D2[(i + 1) * p + (p - 1)];
+                const double db = a.D2[(j + 1) * p + 0], dt = a.D2[(j + 1) * p + (p - 1)];
+                const double2 ul = UB[3 * q + j], ur = UB[q + j], ub = UB[i], ut = UB[2 * q + i];
+                v.x -= a.c2 * (dl * ul.x + dr * ur.x + db * ub.x + dt * ut.x);
+                v.y -= a.c2 * (dl * ul.y + dr * ur.y + db * ub.y + dt * ut.y);
+            }
+        }
+        P[i * FDM_LDD + j] = v;
+    }
+    __syncwarp();
+
+    double cr[2][2][2], ci[2][2][2];
+    // stage 1: S1 = Vinv T            (contract i)        -> Q[i'][j]
+    fdm_stage<false, FDM_LDD>(vif, P, g, t4, cr, ci);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                Q[(mt * 8 + g) * FDM_LDT + nt * 8 + 2 * t4 + c] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
+    __syncwarp();
+    // stage 2: S2^T = Vinv S1^T       (contract j) -> C[j'][i'], scaled by Dinv (symmetric) -> R[j'][i']
+    fdm_stage<true, FDM_LDT>(vif, Q, g, t4, cr, ci);
+    const double2* dv = a.Dinv + (size_t)m * FDM_T * FDM_T;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int jp = mt * 8 + g, ip = nt * 8 + 2 * t4 + c;
+                const double2 d = __ldg(dv + ip * FDM_T + jp);
+                const double xr = cr[mt][nt][c], xi = ci[mt][nt][c];
+                R[jp * FDM_LDT + ip] = make_double2(xr * d.x - xi * d.y, xr * d.y + xi * d.x);
+            }
+    __syncwarp();
+    // stage 3: S3 = V W               (contract i'), W[i'][j'] = R[j'][i']  -> Q[i][j']
+    fdm_stage<true, FDM_LDT>(vf, R, g, t4, cr, ci);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                Q[(mt * 8 + g) * FDM_LDT + nt * 8 + 2 * t4 + c] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
+    __syncwarp();
+    // stage 4: U^T = V S3^T           (contract j') -> C[j][i] = U[i][j]
+    fdm_stage<true, FDM_LDT>(vf, Q, g, t4, cr, ci);
+
+    if (MODE == 1) {
+        double2* wl = a.w + (((size_t)m * a.nelem + leaf) * q2) * a.R2 + r2;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int j = mt * 8 + g, i = nt * 8 + 2 * t4 + c;
+                    if (i < q && j < q) wl[(size_t)(j * q + i) * a.R2] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
+                }
+        return;
+    }
+    // UP: keep U in P for the flux h = N_I u
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int j = mt * 8 + g, i = nt * 8 + 2 * t4 + c;
+                P[i * FDM_LDD + j] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
+            }
+    __syncwarp();
+    for (int b = lane; b < nb; b += 32) {
+        const int side = b / q, s1 = b % q;
+        const double* drow = a.D + ((side == 0 || side == 3) ? 0 : (p - 1) * p);
+        const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
+        double sx = 0.0, sy = 0.0;
+        for (int k = 0; k < q; ++k) {
+            // bottom/top: U[i = s1][j = k];  right/left: U[i = k][j = s1]
+            const double2 u = (side == 0 || side == 2) ? P[s1 * FDM_LDD + k] : P[k * FDM_LDD + s1];
+            const double dk = drow[k + 1];
+            sx = fma(dk, u.x, sx);
+            sy = fma(dk, u.y, sy);
+        }
+        a.h[((size_t)m * a.hps + (size_t)leaf * nb + b) * a.R2 + r2] = make_double2(sgn * sx, sgn * sy);
+    }
+}
+
+}  // namespace dev
+}  // namespace rexp

@@ -111,6 +111,10 @@ struct PoleTables {
 };
 void build_pole_tables(const Problem& P, const RationalApprox& ra, PoleTables& pt);
 
+// real eigen-decomposition of a q x q matrix with real spectrum (eig.cpp)
+int real_eig(int q, const std::vector<double>& K, std::vector<double>& lam, std::vector<double>& V,
+             std::vector<double>& Vinv);
+
 // Host HPS factorization of half poles [h0, h1) into ops (levels: 0 leaf, 1..L merges, L+1 root)
 int factor_host(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1,
                 bool shared, int nthreads, std::vector<HostLevelOps>& ops);

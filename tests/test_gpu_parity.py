@@ -51,13 +51,18 @@ def c0():
     return cfg, m, op, u0
 
 
-@pytest.mark.parametrize("store", ["shared", "pernode"])
-def test_config0_full_run_parity(c0, store):
+@pytest.mark.parametrize("store", ["shared", "shared-dense-leaf", "pernode"])
+def test_config0_full_run_parity(c0, store, monkeypatch):
+    """shared: tensor-product leaf inverse + DMMA GEMMs; shared-dense-leaf: dense q^2 x q^2
+    leaf operators (REXP_LEAF=dense); pernode: one operator set per tree node (GEMV path)."""
     cfg, m, op, u0 = c0
     Lam = cfg["Lambda_tau"] / cfg["tau"]
-    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], store=store)
+    if store == "shared-dense-leaf":
+        monkeypatch.setenv("REXP_LEAF", "dense")
+    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"],
+                     store="pernode" if store == "pernode" else "shared")
     assert h.num_poles == len(op.poles)
-    nst = cfg["nsteps"] if store == "shared" else 3
+    nst = cfg["nsteps"] if store != "pernode" else 3
     got = _gpu_apply(h, u0, nst)
     ref = op.evolve(u0, nst)
     err = rel_l2(got, ref)
