@@ -17,6 +17,7 @@
 // to NB nodes, so each 16-byte load feeds NB*R2 complex FMAs.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
@@ -498,6 +499,55 @@ __global__ void k_pole_sum(PoleSumArgs a) {
 }
 
 // --------------------------------------------------------------------------
+// k_pole_sum_fused (tensor-product leaf path): interior nodes combine the
+// pole-group partials written by k_leaf_fdm<2> (group order), edge nodes sum
+// their per-pole values (ascending pole order).
+// --------------------------------------------------------------------------
+struct PoleSum2Args {
+    const double* Epart;    // [ngroups][nE][R2][NI]
+    const double2* edge;    // [nh][NE][R2]
+    const double2* dE;      // [nh][nE]
+    double* E;              // [nE][R2][N]
+    long long N, NI, NE;
+    int nh, nE, R2, ngroups;
+};
+
+__global__ void k_pole_sum_fused(PoleSum2Args a) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (tid >= a.N * a.R2) return;
+    const long long g = tid % a.N;
+    const int r2 = (int)(tid / a.N);
+    double s[3] = {0.0, 0.0, 0.0};
+    if (g < a.NI) {
+        for (int grp = 0; grp < a.ngroups; ++grp)
+            for (int k = 0; k < a.nE; ++k) s[k] += a.Epart[(((size_t)grp * a.nE + k) * a.R2 + r2) * a.NI + g];
+    } else {
+        const double2* base = a.edge + (g - a.NI) * a.R2 + r2;
+        const long long ps = a.NE * a.R2;
+        int m = 0;
+        for (; m + 4 <= a.nh; m += 4) {
+            double2 u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = base[(size_t)(m + k) * ps];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                for (int e = 0; e < a.nE; ++e) {
+                    const double2 d = a.dE[(size_t)(m + k) * a.nE + e];
+                    s[e] += d.x * u[k].x - d.y * u[k].y;
+                }
+        }
+        for (; m < a.nh; ++m) {
+            const double2 u = base[(size_t)m * ps];
+            for (int e = 0; e < a.nE; ++e) {
+                const double2 d = a.dE[(size_t)m * a.nE + e];
+                s[e] += d.x * u.x - d.y * u.y;
+            }
+        }
+    }
+    for (int k = 0; k < a.nE; ++k) a.E[((size_t)k * a.R2 + r2) * a.N + g] = s[k];
+}
+
+// --------------------------------------------------------------------------
 // k_recover: new state from pole sums (velocity recovery, fused with the sum's output)
 // --------------------------------------------------------------------------
 struct RecoverArgs {
@@ -829,7 +879,22 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         return alloc(pp, count);
     };
     if ((rc = walloc(&d_F, static_cast<size_t>(NI) * nF * R2, 8))) return rc;
-    if ((rc = walloc(&d_w, static_cast<size_t>(nh) * NI * R2, 16))) return rc;
+    {
+        const char* env = std::getenv("REXP_FUSE_SUM");
+        fuse_sum = env && std::string(env) == "1";
+    }
+    if (!fdm || !fuse_sum) {
+        if ((rc = walloc(&d_w, static_cast<size_t>(nh) * NI * R2, 16))) return rc;
+    }
+    if (fdm && fuse_sum) {
+        // pole groups for the fused downward leaf solve + interior pole sum:
+        // enough (leaf, part, group) warps to fill ~2 waves of 148 SMs x 16 warps
+        const long long per_group = static_cast<long long>(nelem) * R2;
+        ngroups = static_cast<int>(std::min<long long>(nh, std::max<long long>(1, (4736 + per_group - 1) / per_group)));
+        pgroup = (nh + ngroups - 1) / ngroups;
+        ngroups = (nh + pgroup - 1) / pgroup;
+        if ((rc = walloc(&d_Epart, static_cast<size_t>(ngroups) * nE * R2 * NI, 8))) return rc;
+    }
     if ((rc = walloc(&d_edge, static_cast<size_t>(nh) * NE * R2, 16))) return rc;
     size_t hmax = static_cast<size_t>(nelem) * nb;
     for (auto& L : T.levels) hmax = std::max(hmax, static_cast<size_t>(L.nodes) * L.next);
@@ -998,6 +1063,7 @@ void cg_tile(int rows, int ncols, int& MT, int& WN) {
 void DeviceStore::configure_kernels() {
     cudaFuncSetAttribute(k_leaf_fdm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_fdm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_fdm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cg_allow_r2<2>();
     cg_allow_r2<4>();
@@ -1038,10 +1104,11 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         fd.V = d_V; fd.Vinv = d_Vinv; fd.Dinv = d_Dinv; fd.D = d_D; fd.D2 = d_D2; fd.F = d_F; fd.cF = d_cF;
         fd.q = q; fd.p = p; fd.nF = nF; fd.nelem = nelem; fd.R2 = R2; fd.nh = nh; fd.c1 = c1; fd.c2 = c1 * c1;
         fd.h = d_h[0]; fd.hps = hstride; fd.edge = d_edge; fd.NE = NE; fd.gB = d_leaf_gB; fd.w = d_w;
+        fd.dE = d_dE; fd.nE = nE; fd.pgroup = pgroup; fd.ngroups = ngroups; fd.Epart = d_Epart;
     }
     const long long nprob = static_cast<long long>(nh) * nelem * R2;
     const unsigned fdm_blocks = static_cast<unsigned>((nprob + FDM_WARPS - 1) / FDM_WARPS);
-    const size_t fdm_smem = static_cast<size_t>(FDM_WARPS) * FDM_TILE_ELEMS * sizeof(double2);
+    const size_t fdm_smem = (static_cast<size_t>(FDM_WARPS) * FDM_TILE_ELEMS + FDM_T * FDM_LDV) * sizeof(double2);
     if (fdm) {
         tbeg(s);
         k_leaf_fdm<0><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
@@ -1173,7 +1240,13 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         tend(T_MERGE_DOWN, s);
     }
     // leaves down
-    if (fdm) {
+    if (fdm && fuse_sum) {
+        // downward leaf solves fused with the interior pole sums (u_m stays on chip)
+        const long long nsum = static_cast<long long>(ngroups) * nelem * R2;
+        tbeg(s);
+        k_leaf_fdm<2><<<static_cast<unsigned>((nsum + FDM_WARPS - 1) / FDM_WARPS), 32 * FDM_WARPS, fdm_smem, s>>>(fd);
+        tend(T_LEAF_DOWN, s);
+    } else if (fdm) {
         tbeg(s);
         k_leaf_fdm<1><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
         tend(T_LEAF_DOWN, s);
@@ -1206,6 +1279,16 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
 }
 
 int DeviceStore::pole_sum(double* d_E_out, cudaStream_t s) {
+    if (fdm && fuse_sum) {
+        PoleSum2Args a{};
+        a.Epart = d_Epart; a.edge = d_edge; a.dE = d_dE; a.E = d_E_out;
+        a.N = N; a.NI = NI; a.NE = NE; a.nh = nh; a.nE = nE; a.R2 = R2; a.ngroups = ngroups;
+        const long long tot = N * R2;
+        tbeg(s);
+        k_pole_sum_fused<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
+        tend(T_POLE_SUM, s);
+        return check("pole_sum");
+    }
     PoleSumArgs a{};
     a.w = d_w; a.edge = d_edge; a.dE = d_dE; a.E = d_E_out;
     a.N = N; a.NI = NI; a.NE = NE; a.nh = nh; a.nE = nE; a.R2 = R2;

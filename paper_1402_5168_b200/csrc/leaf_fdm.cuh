@@ -42,6 +42,10 @@ struct FdmArgs {
     long long NE;
     const int* gB;          // [nelem][4q]
     double2* w;             // [nh][nelem][q2][R2]
+    // DOWN_SUM
+    const double2* dE;      // [nh][nE]
+    int nE, pgroup, ngroups;
+    double* Epart;          // [ngroups][nE][R2][NI]
 };
 
 __device__ __forceinline__ void dmma884r(double& c0, double& c1, double a, double b) {
@@ -52,8 +56,10 @@ __device__ __forceinline__ void dmma884r(double& c0, double& c1, double a, doubl
 
 // C (16x16 complex, in fragments) = A (16x16 real, fragments af) * B, where
 // B[k][n] = TRANS ? X[n*LD + k] : X[k*LD + n]  (complex tile in shared memory).
+constexpr int FDM_LDV = 18;        // stride of V, V^-1 in shared memory
+
 template <bool TRANS, int LD>
-__device__ __forceinline__ void fdm_stage(const double (&af)[2][4], const double2* X, int g, int t4,
+__device__ __forceinline__ void fdm_stage(const double* As, const double2* X, int g, int t4,
                                           double (&cr)[2][2][2], double (&ci)[2][2][2]) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -62,6 +68,9 @@ __device__ __forceinline__ void fdm_stage(const double (&af)[2][4], const double
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
         const int k = ks * 4 + t4;
+        double af[2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) af[mt] = As[(mt * 8 + g) * FDM_LDV + k];   // A[m][k]
         double2 b[2];
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
@@ -71,62 +80,65 @@ __device__ __forceinline__ void fdm_stage(const double (&af)[2][4], const double
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) dmma884r(cr[mt][nt][0], cr[mt][nt][1], af[mt][ks], b[nt].x);
+            for (int mt = 0; mt < 2; ++mt) dmma884r(cr[mt][nt][0], cr[mt][nt][1], af[mt], b[nt].x);
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) dmma884r(ci[mt][nt][0], ci[mt][nt][1], af[mt][ks], b[nt].y);
+            for (int mt = 0; mt < 2; ++mt) dmma884r(ci[mt][nt][0], ci[mt][nt][1], af[mt], b[nt].y);
     }
 }
 
-template <int MODE>   // 0 = UP, 1 = DOWN
-__global__ void __launch_bounds__(32 * FDM_WARPS) k_leaf_fdm(FdmArgs a) {
-    extern __shared__ double2 fsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Right-hand side tile T (UP: f; DOWN: f - A_IB u_B) for pole m, then the
+// four stages; returns U[i][j] in fragments (cr, ci) at (j = mt*8+g, i = nt*8+2t4+c).
+template <bool DOWN>
+__device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int r2, int lane, double2* P, double2* Q,
+                                          double2* UB, const double* vf, const double* vif,
+                                          double (&cr)[2][2][2], double (&ci)[2][2][2]) {
     const int g = lane >> 2, t4 = lane & 3;
-    const long long prob = (long long)blockIdx.x * FDM_WARPS + warp;
-    const long long nprob = (long long)a.nh * a.nelem * a.R2;
-    if (prob >= nprob) return;
-    const int r2 = (int)(prob % a.R2);
-    const int leaf = (int)((prob / a.R2) % a.nelem);
-    const int m = (int)(prob / ((long long)a.R2 * a.nelem));
     const int q = a.q, p = a.p, q2 = q * q, nb = 4 * q;
-    double2* P = fsm + (size_t)warp * FDM_TILE_ELEMS;      // T, then S2^T (scaled), then U
-    double2* Q = P + FDM_T * FDM_LDT;                       // S1, then S3
-    double2* R = P;
-    double2* UB = Q + FDM_T * FDM_LDT;                      // boundary values (DOWN), 4q <= 64
-
-    // A fragments: af[mt][ks] = A[mt*8 + g][ks*4 + t4]
-    double vf[2][4], vif[2][4];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-            vf[mt][ks] = __ldg(a.V + (mt * 8 + g) * FDM_T + ks * 4 + t4);
-            vif[mt][ks] = __ldg(a.Vinv + (mt * 8 + g) * FDM_T + ks * 4 + t4);
-        }
-
-    // ---- right-hand side T = f (UP) or f - A_IB u_B (DOWN), zero padded ----
     const double2* cf = a.cF + (size_t)m * a.nF;
     const double2 c0 = cf[0];
     const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0, 0);
     const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0, 0);
-    if (MODE == 1) {
-        for (int b = lane; b < nb; b += 32)
-            UB[b] = a.edge[((size_t)m * a.NE + a.gB[(size_t)leaf * nb + b]) * a.R2 + r2];
+    // issue every global load of this problem up front (boundary values, the
+    // pole-independent fields of the 8 tile elements this lane forms)
+    double2 ubv[2];
+    if (DOWN) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int b = lane + 32 * u;
+            ubv[u] = b < nb ? a.edge[((size_t)m * a.NE + a.gB[(size_t)leaf * nb + b]) * a.R2 + r2]
+                            : make_double2(0.0, 0.0);
+        }
+    }
+    double fv[8][3];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int e = lane + 32 * u;
+        const int i = e % FDM_T, j = e / FDM_T;
+        fv[u][0] = fv[u][1] = fv[u][2] = 0.0;
+        if (i < q && j < q) {
+            const double* f = a.F + ((size_t)((size_t)leaf * q2 + j * q + i) * a.nF) * a.R2 + r2;
+            fv[u][0] = f[0];
+            if (a.nF > 1) fv[u][1] = f[a.R2];
+            if (a.nF > 2) fv[u][2] = f[2 * a.R2];
+        }
+    }
+    if (DOWN) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (lane + 32 * u < nb) UB[lane + 32 * u] = ubv[u];
         __syncwarp();
     }
-    for (int e = lane; e < FDM_T * FDM_T; e += 32) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int e = lane + 32 * u;
         const int i = e % FDM_T, j = e / FDM_T;
         double2 v = make_double2(0.0, 0.0);
         if (i < q && j < q) {
-            const double* f = a.F + ((size_t)((size_t)leaf * q2 + j * q + i) * a.nF) * a.R2 + r2;
-            const double f0 = f[0];
-            const double f1 = a.nF > 1 ? f[a.R2] : 0.0;
-            const double f2 = a.nF > 2 ? f[2 * a.R2] : 0.0;
-            v.x = c0.x * f0 + c1v.x * f1 + c2v.x * f2;
-            v.y = c0.y * f0 + c1v.y * f1 + c2v.y * f2;
-            if (MODE == 1) {
+            v.x = c0.x * fv[u][0] + c1v.x * fv[u][1] + c2v.x * fv[u][2];
+            v.y = c0.y * fv[u][0] + c1v.y * fv[u][1] + c2v.y * fv[u][2];
+            if (DOWN) {
                 // A_IB u_B at interior (i+1, j+1): row i+1 meets left/right, column j+1 meets bottom/top
                 const double dl = a.D2[(i + 1) * p + 0], dr = a.D2[(i + 1) * p + (p - 1)];
                 const double db = a.D2[(j + 1) * p + 0], dt = a.D2[(j + 1) * p + (p - 1)];
@@ -138,8 +150,15 @@ __global__ void __launch_bounds__(32 * FDM_WARPS) k_leaf_fdm(FdmArgs a) {
         P[i * FDM_LDD + j] = v;
     }
     __syncwarp();
-
-    double cr[2][2][2], ci[2][2][2];
+    // D^-1 entries of this lane's stage-2 fragments, fetched while stages 1-2 run
+    const double2* dv = a.Dinv + (size_t)m * FDM_T * FDM_T;
+    double2 dinv[2][2][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) dinv[mt][nt][c] = __ldg(dv + (nt * 8 + 2 * t4 + c) * FDM_T + mt * 8 + g);
     // stage 1: S1 = Vinv T            (contract i)        -> Q[i'][j]
     fdm_stage<false, FDM_LDD>(vif, P, g, t4, cr, ci);
 #pragma unroll
@@ -150,9 +169,8 @@ __global__ void __launch_bounds__(32 * FDM_WARPS) k_leaf_fdm(FdmArgs a) {
             for (int c = 0; c < 2; ++c)
                 Q[(mt * 8 + g) * FDM_LDT + nt * 8 + 2 * t4 + c] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
     __syncwarp();
-    // stage 2: S2^T = Vinv S1^T       (contract j) -> C[j'][i'], scaled by Dinv (symmetric) -> R[j'][i']
+    // stage 2: S2^T = Vinv S1^T       (contract j) -> C[j'][i'], scaled by Dinv (symmetric) -> P[j'][i']
     fdm_stage<true, FDM_LDT>(vif, Q, g, t4, cr, ci);
-    const double2* dv = a.Dinv + (size_t)m * FDM_T * FDM_T;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -160,13 +178,13 @@ __global__ void __launch_bounds__(32 * FDM_WARPS) k_leaf_fdm(FdmArgs a) {
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int jp = mt * 8 + g, ip = nt * 8 + 2 * t4 + c;
-                const double2 d = __ldg(dv + ip * FDM_T + jp);
+                const double2 d = dinv[mt][nt][c];
                 const double xr = cr[mt][nt][c], xi = ci[mt][nt][c];
-                R[jp * FDM_LDT + ip] = make_double2(xr * d.x - xi * d.y, xr * d.y + xi * d.x);
+                P[jp * FDM_LDT + ip] = make_double2(xr * d.x - xi * d.y, xr * d.y + xi * d.x);
             }
     __syncwarp();
-    // stage 3: S3 = V W               (contract i'), W[i'][j'] = R[j'][i']  -> Q[i][j']
-    fdm_stage<true, FDM_LDT>(vf, R, g, t4, cr, ci);
+    // stage 3: S3 = V W               (contract i'), W[i'][j'] = P[j'][i']  -> Q[i][j']
+    fdm_stage<true, FDM_LDT>(vf, P, g, t4, cr, ci);
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -177,6 +195,90 @@ __global__ void __launch_bounds__(32 * FDM_WARPS) k_leaf_fdm(FdmArgs a) {
     __syncwarp();
     // stage 4: U^T = V S3^T           (contract j') -> C[j][i] = U[i][j]
     fdm_stage<true, FDM_LDT>(vf, Q, g, t4, cr, ci);
+    __syncwarp();   // P, Q reusable by the caller after this point
+}
+
+// MODE 0 = UP (h = N_I A^-1 f), 1 = DOWN (interior solution u_m written),
+// 2 = DOWN_SUM: a warp walks the half poles [grp*pg, grp*pg + pg) for one
+// (leaf, part) and accumulates the interior pole sums E_k = sum_m Re(d_mk u_m)
+// in ascending pole order (u_m never leaves the SM); partials per group.
+template <int MODE>
+__global__ void __launch_bounds__(32 * FDM_WARPS, 2) k_leaf_fdm(FdmArgs a) {
+    extern __shared__ double2 fsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int q = a.q, p = a.p, q2 = q * q, nb = 4 * q;
+    // V, V^-1 once per CTA (padded stride), then per-warp tiles
+    double* vf = reinterpret_cast<double*>(fsm);
+    double* vif = vf + FDM_T * FDM_LDV;
+    for (int e = threadIdx.x; e < FDM_T * FDM_T; e += blockDim.x) {
+        const int r = e / FDM_T, c = e % FDM_T;
+        vf[r * FDM_LDV + c] = a.V[e];
+        vif[r * FDM_LDV + c] = a.Vinv[e];
+    }
+    __syncthreads();
+    double2* P = fsm + FDM_T * FDM_LDV + (size_t)warp * FDM_TILE_ELEMS;   // 2*16*18 doubles = 16*18 double2
+    double2* Q = P + FDM_T * FDM_LDT;
+    double2* UB = Q + FDM_T * FDM_LDT;
+    double cr[2][2][2], ci[2][2][2];
+    const long long prob = (long long)blockIdx.x * FDM_WARPS + warp;
+
+    if (MODE == 2) {
+        const long long nprob = (long long)a.ngroups * a.nelem * a.R2;
+        if (prob >= nprob) return;
+        const int r2 = (int)(prob % a.R2);
+        const int leaf = (int)((prob / a.R2) % a.nelem);
+        const int grp = (int)(prob / ((long long)a.R2 * a.nelem));
+        const int m0 = grp * a.pgroup, m1 = min(a.nh, m0 + a.pgroup);
+        double E[3][2][2][2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) E[k][mt][nt][0] = E[k][mt][nt][1] = 0.0;
+        for (int m = m0; m < m1; ++m) {
+            fdm_solve<true>(a, m, leaf, r2, lane, P, Q, UB, vf, vif, cr, ci);
+            const double2* dm = a.dE + (size_t)m * a.nE;
+            const double2 d0 = dm[0], d1 = dm[1];
+            const double2 d2 = a.nE > 2 ? dm[2] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const double ur = cr[mt][nt][c], ui = ci[mt][nt][c];
+                        E[0][mt][nt][c] += d0.x * ur - d0.y * ui;
+                        E[1][mt][nt][c] += d1.x * ur - d1.y * ui;
+                        E[2][mt][nt][c] += d2.x * ur - d2.y * ui;
+                    }
+        }
+        // partial sums of this pole group at the leaf's interior nodes
+        const size_t NI = (size_t)a.nelem * q2;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int j = mt * 8 + g, i = nt * 8 + 2 * t4 + c;
+                    if (i < q && j < q) {
+                        const size_t node = (size_t)leaf * q2 + j * q + i;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k)
+                            if (k < a.nE) a.Epart[(((size_t)grp * a.nE + k) * a.R2 + r2) * NI + node] = E[k][mt][nt][c];
+                    }
+                }
+        return;
+    }
+
+    const long long nprob = (long long)a.nh * a.nelem * a.R2;
+    if (prob >= nprob) return;
+    const int r2 = (int)(prob % a.R2);
+    const int leaf = (int)((prob / a.R2) % a.nelem);
+    const int m = (int)(prob / ((long long)a.R2 * a.nelem));
+    fdm_solve<MODE == 1>(a, m, leaf, r2, lane, P, Q, UB, vf, vif, cr, ci);
 
     if (MODE == 1) {
         double2* wl = a.w + (((size_t)m * a.nelem + leaf) * q2) * a.R2 + r2;
@@ -191,8 +293,7 @@ __global__ void __launch_bounds__(32 * FDM_WARPS) k_leaf_fdm(FdmArgs a) {
                 }
         return;
     }
-    // UP: keep U in P for the flux h = N_I u
-    __syncwarp();
+    // UP: U into P, then the flux h = N_I u
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
