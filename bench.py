@@ -277,7 +277,7 @@ def run_ours(args, cfg):
     t_setup = time.perf_counter() - t_setup
     x, y = h.node_coords()
     N = h.N
-    u0 = np.stack([initial_state(cfg["model"], x, y, cfg["seed"] + k) for k in range(cfg["nrhs"])])
+    u0 = np.stack([initial_state(cfg["model"], x, y, cfg["seed"] + 10 * k) for k in range(cfg["nrhs"])])
     u = torch.from_numpy(u0).to(dev).contiguous()
     stream = torch.cuda.current_stream(dev)
     e = torch.zeros(h.partial_len, dtype=torch.float64, device=dev) if world > 1 else None

@@ -89,7 +89,8 @@ typedef struct rexp_problem {
 } rexp_problem;
 
 typedef struct rexp_options {
-    int32_t nrhs;         /* independent complex states applied together: 1..4          */
+    int32_t nrhs;         /* independent complex states applied together: 1..64
+                             (per-node store: 1..4)                                      */
     int32_t store;        /* REXP_STORE_*                                               */
     int32_t device;       /* CUDA ordinal for the operator store; -1 = host-only build
                              (operators kept on the host for rexp_export_*; rexp_apply

@@ -1,6 +1,7 @@
 // C ABI of include/rexp.h.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -73,8 +74,8 @@ int rexp_setup(const rexp_problem* prob, double tau, double delta, double Lambda
         set_error("rexp_setup: tau, Lambda, delta must be positive");
         return REXP_EINVAL;
     }
-    if (opt.nrhs != 1 && opt.nrhs != 2 && opt.nrhs != 4) {
-        set_error("rexp_setup: nrhs must be 1, 2 or 4");
+    if (opt.nrhs < 1 || opt.nrhs > 64) {
+        set_error("rexp_setup: nrhs must be in 1..64");
         return REXP_EINVAL;
     }
     if (prob->p > 18) {
@@ -121,9 +122,13 @@ int rexp_setup(const rexp_problem* prob, double tau, double delta, double Lambda
     h->shared = store == REXP_STORE_SHARED;
     h->nrhs = opt.nrhs;
     h->device = opt.device;
-    std::vector<HostLevelOps> ops;
-    if ((rc = factor_host(h->P, h->T, h->pt, h->h0, h->h1, h->shared, opt.nthreads, ops))) return rc;
+    if (!h->shared && opt.nrhs > 4) {
+        set_error("rexp_setup: the per-node store supports nrhs <= 4");
+        return REXP_EINVAL;
+    }
     if (opt.device < 0) {
+        std::vector<HostLevelOps> ops;
+        if ((rc = factor_host(h->P, h->T, h->pt, h->h0, h->h1, h->shared, opt.nthreads, ops))) return rc;
         h->host_ops = std::move(ops);
     } else {
         int ndev = 0;
@@ -137,7 +142,17 @@ int rexp_setup(const rexp_problem* prob, double tau, double delta, double Lambda
             return REXP_ENODEV;
         }
         h->dev.reset(new dev::DeviceStore());
-        if ((rc = h->dev->init(h->P, h->T, h->pt, h->h0, h->h1, h->shared, h->nrhs, ops))) return rc;
+        if ((rc = h->dev->init(h->P, h->T, h->pt, h->h0, h->h1, h->shared, h->nrhs))) return rc;
+        // factor on the host and upload in pole chunks of <= ~8 GB of operators
+        const int64_t nhl = h->h1 - h->h0;
+        const int64_t per_pole = std::max<int64_t>(1, h->dev->store_bytes / std::max<int64_t>(1, nhl));
+        const int64_t cmax = std::max<int64_t>(1, (int64_t(8) << 30) / per_pole);
+        for (int c0 = h->h0; c0 < h->h1; c0 += static_cast<int>(cmax)) {
+            const int c1 = static_cast<int>(std::min<int64_t>(h->h1, c0 + cmax));
+            std::vector<HostLevelOps> ops;
+            if ((rc = factor_host(h->P, h->T, h->pt, c0, c1, h->shared, opt.nthreads, ops))) return rc;
+            if ((rc = h->dev->upload_ops(ops, c0 - h->h0))) return rc;
+        }
     }
     *out = h.release();
     return REXP_OK;
@@ -205,9 +220,7 @@ int64_t rexp_partial_len(const rexp_handle* h) {
 int rexp_step_partial(rexp_handle* h, const double* u_dev, double* e_dev, void* stream) {
     int rc = need_device(h, false);
     if (rc) return rc;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if ((rc = h->dev->solve_poles(u_dev, s))) return rc;
-    return h->dev->pole_sum(e_dev, s);
+    return h->dev->solve_sum(u_dev, e_dev, static_cast<cudaStream_t>(stream));
 }
 
 int rexp_step_finish(rexp_handle* h, const double* e_dev, double* u_dev, void* stream) {

@@ -16,11 +16,12 @@
 namespace rexp {
 namespace dev {
 
-enum CgemmMode { CG_LEAF_UP = 0, CG_LEAF_DOWN = 1, CG_UPX = 2, CG_UPY = 3, CG_DOWN = 4 };
+enum CgemmMode { CG_LEAF_UP = 0, CG_LEAF_DOWN = 1, CG_UPX = 2, CG_UPY = 3, CG_DOWN = 4, CG_ROOT = 5 };
 
 struct CgemmArgs {
     const double2* A;       // [nh][rows*K] column-major (shared store)
     int rows, K, nodes;
+    int R2;                 // real right-hand sides per node (used when the template R2 is 0)
     int nrowblk;
     // LEAF_UP
     const double* F;        // [NI][nF][R2]
@@ -58,18 +59,21 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // turns them into the B element (after the math).
 struct BRaw { double v[4]; };
 
-template <int R2, int MODE>
+template <int R2T, int MODE>
 __device__ __forceinline__ void cg_fetch(const CgemmArgs& a, int m, int k, int col, BRaw& r) {
+    const int R2 = R2T ? R2T : a.R2;
     const int node = col / R2, r2 = col % R2;
     if (MODE == CG_LEAF_UP) {
         const double* f = a.F + ((size_t)(node * a.q2 + k) * a.nF) * R2 + r2;
         r.v[0] = f[0];
         r.v[1] = a.nF > 1 ? f[R2] : 0.0;
         r.v[2] = a.nF > 2 ? f[2 * R2] : 0.0;
-    } else if (MODE == CG_UPX) {
+    } else if (MODE == CG_UPX || MODE == CG_ROOT) {
+        // ROOT: one node, node-independent seam positions pos1/pos2 (P^T h)
         const double2* s = a.src + (size_t)m * a.src_ps * R2;
-        const double2 v0 = s[(size_t)a.bi0[(size_t)node * a.K + k] * R2 + r2];
-        const double2 v1 = s[(size_t)a.bi1[(size_t)node * a.K + k] * R2 + r2];
+        const size_t o = MODE == CG_ROOT ? (size_t)k : (size_t)node * a.K + k;
+        const double2 v0 = s[(size_t)a.bi0[o] * R2 + r2];
+        const double2 v1 = s[(size_t)a.bi1[o] * R2 + r2];
         r.v[0] = v0.x; r.v[1] = v0.y; r.v[2] = v1.x; r.v[3] = v1.y;
     } else if (MODE == CG_UPY) {
         const double2 v = a.src[(size_t)m * a.src_ps * R2 + ((size_t)node * a.K + k) * R2 + r2];
@@ -87,15 +91,16 @@ __device__ __forceinline__ double2 cg_form(const BRaw& r, const double2* cf) {
         v.x = fma(cf[0].x, r.v[0], fma(cf[1].x, r.v[1], cf[2].x * r.v[2]));
         v.y = fma(cf[0].y, r.v[0], fma(cf[1].y, r.v[1], cf[2].y * r.v[2]));
         return v;
-    } else if (MODE == CG_UPX) {
+    } else if (MODE == CG_UPX || MODE == CG_ROOT) {
         return make_double2(r.v[0] + r.v[2], r.v[1] + r.v[3]);
     } else {
         return make_double2(r.v[0], r.v[1]);
     }
 }
 
-template <int R2, int MODE>
+template <int R2T, int MODE>
 __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int col, double2 v) {
+    const int R2 = R2T ? R2T : a.R2;
     const int node = col / R2, r2 = col % R2;
     if (MODE == CG_LEAF_UP) {
         a.dst[(((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2] = v;
@@ -107,6 +112,8 @@ __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int
         const double2 ad = a.add[((size_t)m * a.add_ps + a.ai0[(size_t)node * a.rows + row]) * R2 + r2];
         a.dst[(size_t)m * a.dst_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2] =
             make_double2(ad.x + v.x, ad.y + v.y);
+    } else if (MODE == CG_ROOT) {   // seam values into the pole's edge array
+        a.dst[((size_t)m * a.dst_ps + a.so0[row]) * R2 + r2] = v;
     } else {  // DOWN (additive w3 folded in by the caller)
         a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * a.rows + row]) * R2 + r2] = v;
     }
@@ -118,9 +125,10 @@ constexpr size_t cgemm_smem_bytes() {
 }
 
 // MT m-tiles and NTW n-tiles per warp; WN warps side by side in n.
-template <int MT, int WN, int BK, int R2, int MODE, int NTW = 1, int MINB = 1>
+template <int MT, int WN, int BK, int R2T, int MODE, int NTW = 1, int MINB = 1>
 __global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
     constexpr int BM = 8 * MT, BN = 8 * WN * NTW, NT = 32 * WN;
+    const int R2 = R2T ? R2T : a.R2;
     static_assert(BK % 4 == 0, "BK must be a multiple of the DMMA k (4)");
     constexpr int LDA = BM + 2, LDB = BN + 2;
     constexpr int BPT = (BK * BN + NT - 1) / NT;     // B elements per thread per chunk
@@ -163,7 +171,7 @@ __global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
             const int kk = e / BN, c = e % BN;
             const int k = k0 + kk, col = col0 + c;
             braw[u].v[0] = braw[u].v[1] = braw[u].v[2] = braw[u].v[3] = 0.0;
-            if (e < BK * BN && k < a.K && col < ncols) cg_fetch<R2, MODE>(a, m, k, col, braw[u]);
+            if (e < BK * BN && k < a.K && col < ncols) cg_fetch<R2T, MODE>(a, m, k, col, braw[u]);
         }
     };
     auto store_B = [&](int buf) {
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
                     v.x += addv[i][n][j].x;
                     v.y += addv[i][n][j].y;
                 }
-                cg_store<R2, MODE>(a, m, row, col, v);
+                cg_store<R2T, MODE>(a, m, row, col, v);
             }
     }
 }

@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(256) k_leaf_down(LeafDownArgs a) {
 // k_pole_sum: E[k][r2][g] = sum_m Re(dE[m][k] * u_m[g][r2])
 // --------------------------------------------------------------------------
 struct PoleSumArgs {
+    int accumulate;         // 1: add to the existing E (pole chunks after the first)
     const double2* w;       // interior solutions [nh][NI][R2]
     const double2* edge;    // edge solutions     [nh][NE][R2]
     const double2* dE;      // [nh][nE]
@@ -461,6 +462,11 @@ __global__ void k_pole_sum(PoleSumArgs a) {
     const long long g = tid / a.R2;
     const int r2 = (int)(tid % a.R2);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (a.accumulate) {
+        s0 = a.E[((size_t)0 * a.R2 + r2) * a.N + g];
+        s1 = a.E[((size_t)1 * a.R2 + r2) * a.N + g];
+        if (a.nE > 2) s2 = a.E[((size_t)2 * a.R2 + r2) * a.N + g];
+    }
     const bool inter = g < a.NI;
     const double2* base = inter ? (a.w + g * a.R2 + r2) : (a.edge + (g - a.NI) * a.R2 + r2);
     const long long ps = (inter ? a.NI : a.NE) * a.R2;
@@ -752,7 +758,7 @@ int DeviceStore::put(T** p, const std::vector<T>& v) {
 }
 
 int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int h0_, int h1_, bool shared_,
-                      int nrhs_, const std::vector<HostLevelOps>& ops) {
+                      int nrhs_) {
     model = P.model;
     n = T.n; p = T.p; q = T.q; q2 = q * q; nb = 4 * q;
     N = T.N; NI = T.NI; NV = T.NV; NE = T.NE; nelem = T.nelem;
@@ -765,30 +771,18 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     c1 = 2.0 * n;
     scal = pt.scal;
     int rc;
+    if (!shared && R2 > 8) {
+        set_error("the per-node store supports nrhs <= 4");
+        return REXP_EINVAL;
+    }
     // mesh data
     const Cheb ch = make_cheb(p);
     if ((rc = put(&d_D, ch.D))) return rc;
     if ((rc = put(&d_Dw, ch.Dw))) return rc;
+    if ((rc = put(&d_D2, ch.D2))) return rc;
     if ((rc = put(&d_elem_g, T.elem_g))) return rc;
     if (model == REXP_MODEL_WAVE) {
         if ((rc = put(&d_kappa, P.kappa))) return rc;
-    }
-    // N_I (pole independent, real): recompute from the leaf geometry
-    {
-        std::vector<double> NIm(static_cast<size_t>(nb) * q2, 0.0);
-        const double* D = ch.D.data();
-        auto I = [this](int i, int j) { return (j - 1) * q + (i - 1); };
-        for (int i = 1; i <= q; ++i)
-            for (int k = 1; k <= p - 2; ++k) {
-                NIm[static_cast<size_t>(i - 1) * q2 + I(i, k)] += -c1 * D[0 * p + k];               // bottom
-                NIm[static_cast<size_t>(2 * q + i - 1) * q2 + I(i, k)] += c1 * D[(p - 1) * p + k];  // top
-            }
-        for (int j = 1; j <= q; ++j)
-            for (int k = 1; k <= p - 2; ++k) {
-                NIm[static_cast<size_t>(q + j - 1) * q2 + I(k, j)] += c1 * D[(p - 1) * p + k];      // right
-                NIm[static_cast<size_t>(3 * q + j - 1) * q2 + I(k, j)] += -c1 * D[0 * p + k];       // left
-            }
-        if ((rc = put(&d_NI, NIm))) return rc;
     }
     // pole tables for this handle's range
     {
@@ -806,22 +800,14 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         if ((rc = put(&d_cF, cF))) return rc;
         if ((rc = put(&d_dE, dE))) return rc;
     }
-    // operators
-    store_bytes = 0;
-    auto put_ops = [&](const std::vector<cd>& v, double2** d) -> int {
-        std::vector<double2> tmp(v.size());
-        for (size_t k = 0; k < v.size(); ++k) tmp[k] = make_double2(v[k].real(), v[k].imag());
-        store_bytes += static_cast<int64_t>(v.size()) * 16;
-        return put(d, tmp);
-    };
     // tensor-product leaf inverse for constant coefficients (RSW shared store),
     // unless REXP_LEAF=dense asks for the dense q^2 x q^2 leaf operators
     {
         const char* env = std::getenv("REXP_LEAF");
         const bool want_dense = env && std::string(env) == "dense";
-        fdm = shared && model == REXP_MODEL_RSW && q <= FDM_T && R2 <= 8 && !want_dense;
+        fdm = shared && model == REXP_MODEL_RSW && q <= FDM_T && !want_dense;
     }
-    if ((rc = put(&d_D2, ch.D2))) return rc;
+    store_bytes = 0;
     if (fdm) {
         std::vector<double> K(static_cast<size_t>(q) * q), lam, V, Vi;
         for (int i = 0; i < q; ++i)
@@ -847,19 +833,28 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         if ((rc = put(&d_Vinv, Vip))) return rc;
         if ((rc = put(&d_Dinv, Dinv))) return rc;
         store_bytes += static_cast<int64_t>(Dinv.size()) * 16;
-    } else {
-        if ((rc = put_ops(ops[0].m[0], &d_Ainv))) return rc;
-        if ((rc = put_ops(ops[0].m[1], &d_Sleaf))) return rc;
     }
+    // operator store, filled by upload_ops (possibly in pole chunks)
+    const size_t leaf_stored = shared ? 1 : static_cast<size_t>(nelem);
+    pp_Ainv = fdm ? 0 : leaf_stored * q2 * q2;
+    pp_Sleaf = fdm ? 0 : leaf_stored * q2 * nb;
+    if ((rc = alloc(&d_Ainv, static_cast<size_t>(nh) * pp_Ainv))) return rc;
+    if ((rc = alloc(&d_Sleaf, static_cast<size_t>(nh) * pp_Sleaf))) return rc;
+    store_bytes += static_cast<int64_t>(nh) * static_cast<int64_t>(pp_Ainv + pp_Sleaf) * 16;
     if ((rc = put(&d_leaf_gB, T.leaf_gB))) return rc;
     levels.resize(T.levels.size());
     for (size_t li = 0; li < T.levels.size(); ++li) {
         const MergeLevel& L = T.levels[li];
         Level& D = levels[li];
         D.nodes = L.nodes; D.n3 = L.n3; D.next = L.next; D.nchild = L.nchild; D.child_nodes = L.child_nodes;
-        if ((rc = put_ops(ops[li + 1].m[0], &D.X))) return rc;
-        if ((rc = put_ops(ops[li + 1].m[1], &D.Y))) return rc;
-        if ((rc = put_ops(ops[li + 1].m[2], &D.S))) return rc;
+        const size_t st = shared ? 1 : static_cast<size_t>(L.nodes);
+        D.ppX = st * L.n3 * L.n3;
+        D.ppY = st * L.next * L.n3;
+        D.ppS = st * L.n3 * L.next;
+        if ((rc = alloc(&D.X, nh * D.ppX))) return rc;
+        if ((rc = alloc(&D.Y, nh * D.ppY))) return rc;
+        if ((rc = alloc(&D.S, nh * D.ppS))) return rc;
+        store_bytes += static_cast<int64_t>(nh) * static_cast<int64_t>(D.ppX + D.ppY + D.ppS) * 16;
         if ((rc = put(&D.ia3, L.ia3))) return rc;
         if ((rc = put(&D.ib3, L.ib3))) return rc;
         if ((rc = put(&D.ext, L.ext))) return rc;
@@ -868,48 +863,85 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     }
     ns = T.ns;
     nroot_b = 4 * T.n * T.q;
-    if ((rc = put_ops(ops.back().m[0], &d_Xroot))) return rc;
+    pp_Xroot = static_cast<size_t>(ns) * ns;
+    if ((rc = alloc(&d_Xroot, nh * pp_Xroot))) return rc;
+    store_bytes += static_cast<int64_t>(nh) * static_cast<int64_t>(pp_Xroot) * 16;
     if ((rc = put(&d_rpos1, T.root_pos1))) return rc;
     if ((rc = put(&d_rpos2, T.root_pos2))) return rc;
     if ((rc = put(&d_rgs, T.root_gs))) return rc;
-    // work buffers
+
+    // work buffers, sized for pole chunks of `chunk` half poles
+    size_t hmax = static_cast<size_t>(nelem) * nb;
+    for (auto& L : T.levels) hmax = std::max(hmax, static_cast<size_t>(L.nodes) * L.next);
+    hstride = static_cast<long long>(hmax);
+    size_t w3_per_pole = 0;
+    for (auto& D : levels) w3_per_pole += static_cast<size_t>(D.nodes) * D.n3;
+    const size_t per_pole = (static_cast<size_t>(NI) + NE + 2 * hmax + w3_per_pole) * R2 * 16;
+    {
+        size_t budget = static_cast<size_t>(16) << 30;   // 16 GiB of per-pole work buffers
+        const char* env = std::getenv("REXP_CHUNK");
+        chunk = env ? std::max(1, std::atoi(env)) : static_cast<int>(std::max<size_t>(1, budget / per_pole));
+        chunk = std::min(chunk, nh);
+    }
+    {
+        const char* env = std::getenv("REXP_FUSE_SUM");
+        fuse_sum = fdm && chunk == nh && env && std::string(env) == "1";
+    }
     work_bytes = 0;
     auto walloc = [&](auto** pp, size_t count, size_t elt) -> int {
         work_bytes += static_cast<int64_t>(count * elt);
         return alloc(pp, count);
     };
+    const size_t pc = static_cast<size_t>(chunk);
     if ((rc = walloc(&d_F, static_cast<size_t>(NI) * nF * R2, 8))) return rc;
-    {
-        const char* env = std::getenv("REXP_FUSE_SUM");
-        fuse_sum = env && std::string(env) == "1";
-    }
-    if (!fdm || !fuse_sum) {
-        if ((rc = walloc(&d_w, static_cast<size_t>(nh) * NI * R2, 16))) return rc;
-    }
-    if (fdm && fuse_sum) {
-        // pole groups for the fused downward leaf solve + interior pole sum:
-        // enough (leaf, part, group) warps to fill ~2 waves of 148 SMs x 16 warps
+    if (!fuse_sum) {
+        if ((rc = walloc(&d_w, pc * NI * R2, 16))) return rc;
+    } else {
+        // pole groups for the fused downward leaf solve + interior pole sum
         const long long per_group = static_cast<long long>(nelem) * R2;
         ngroups = static_cast<int>(std::min<long long>(nh, std::max<long long>(1, (4736 + per_group - 1) / per_group)));
         pgroup = (nh + ngroups - 1) / ngroups;
         ngroups = (nh + pgroup - 1) / pgroup;
         if ((rc = walloc(&d_Epart, static_cast<size_t>(ngroups) * nE * R2 * NI, 8))) return rc;
     }
-    if ((rc = walloc(&d_edge, static_cast<size_t>(nh) * NE * R2, 16))) return rc;
-    size_t hmax = static_cast<size_t>(nelem) * nb;
-    for (auto& L : T.levels) hmax = std::max(hmax, static_cast<size_t>(L.nodes) * L.next);
-    if ((rc = walloc(&d_h[0], static_cast<size_t>(nh) * hmax * R2, 16))) return rc;
-    if ((rc = walloc(&d_h[1], static_cast<size_t>(nh) * hmax * R2, 16))) return rc;
-    hstride = static_cast<long long>(hmax);
+    if ((rc = walloc(&d_edge, pc * NE * R2, 16))) return rc;
+    if ((rc = walloc(&d_h[0], pc * hmax * R2, 16))) return rc;
+    if ((rc = walloc(&d_h[1], pc * hmax * R2, 16))) return rc;
     for (size_t li = 0; li < levels.size(); ++li) {
         Level& D = levels[li];
-        if ((rc = walloc(&D.w3, static_cast<size_t>(nh) * D.nodes * D.n3 * R2, 16))) return rc;
+        if ((rc = walloc(&D.w3, pc * D.nodes * D.n3 * R2, 16))) return rc;
     }
     if ((rc = walloc(&d_E, static_cast<size_t>(nE) * R2 * N, 8))) return rc;
     if ((rc = walloc(&d_u, static_cast<size_t>(nrhs) * 3 * N * 2, 8))) return rc;
-    // allow large dynamic shared memory on the templated kernels
     configure_kernels();
     return REXP_OK;
+}
+
+// copy the host factorization of local half poles [m0, m0 + count) into the store
+int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
+    auto up = [&](const std::vector<cd>& v, double2* dst, size_t per_pole) -> int {
+        if (per_pole == 0 || v.empty()) return REXP_OK;
+        std::vector<double2> tmp(v.size());
+        for (size_t k = 0; k < v.size(); ++k) tmp[k] = make_double2(v[k].real(), v[k].imag());
+        if (cudaMemcpy(dst + static_cast<size_t>(m0) * per_pole, tmp.data(), tmp.size() * sizeof(double2),
+                       cudaMemcpyHostToDevice) != cudaSuccess) {
+            set_error("upload_ops: cudaMemcpy failed");
+            return REXP_ENODEV;
+        }
+        return REXP_OK;
+    };
+    int rc;
+    if (!fdm) {
+        if ((rc = up(ops[0].m[0], d_Ainv, pp_Ainv))) return rc;
+        if ((rc = up(ops[0].m[1], d_Sleaf, pp_Sleaf))) return rc;
+    }
+    for (size_t li = 0; li < levels.size(); ++li) {
+        Level& D = levels[li];
+        if ((rc = up(ops[li + 1].m[0], D.X, D.ppX))) return rc;
+        if ((rc = up(ops[li + 1].m[1], D.Y, D.ppY))) return rc;
+        if ((rc = up(ops[li + 1].m[2], D.S, D.ppS))) return rc;
+    }
+    return up(ops.back().m[0], d_Xroot, pp_Xroot);
 }
 
 // launch helpers -------------------------------------------------------------
@@ -996,71 +1028,84 @@ size_t gemv_smem(const GemvArgs& g, int NB, int R2) {
 }
 
 
-template <int MT, int WN, int BK, int R2, int MODE>
+template <int MT, int WN, int BK, int R2T, int MODE>
 void cg_launch(dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    k_cgemm<MT, WN, BK, R2, MODE><<<grid, 32 * WN, cgemm_smem_bytes<MT, WN, BK>(), s>>>(a);
+    k_cgemm<MT, WN, BK, R2T, MODE><<<grid, 32 * WN, cgemm_smem_bytes<MT, WN, BK>(), s>>>(a);
 }
-template <int WN, int BK, int R2, int MODE>
-void cg_mt(int MT, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    switch (MT) {
-        case 2: cg_launch<2, WN, BK, R2, MODE>(grid, s, a); break;
-        case 4: cg_launch<4, WN, BK, R2, MODE>(grid, s, a); break;
-        default: cg_launch<5, WN, BK, R2, MODE>(grid, s, a); break;
+// merge-level tiles: MT in {2, 4}, WN in {2, 4, 8}; leaf tiles: MT in {4, 5}, WN = 8
+template <int BK, int R2T, int MODE>
+void cg_tiles(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    if (MODE == CG_LEAF_UP || MODE == CG_LEAF_DOWN) {
+        if (MT == 4) cg_launch<4, 8, BK, R2T, MODE>(grid, s, a);
+        else cg_launch<5, 8, BK, R2T, MODE>(grid, s, a);
+        return;
+    }
+    if (MT == 2) {
+        if (WN == 2) cg_launch<2, 2, BK, R2T, MODE>(grid, s, a);
+        else if (WN == 4) cg_launch<2, 4, BK, R2T, MODE>(grid, s, a);
+        else cg_launch<2, 8, BK, R2T, MODE>(grid, s, a);
+    } else {
+        if (WN == 2) cg_launch<4, 2, BK, R2T, MODE>(grid, s, a);
+        else if (WN == 4) cg_launch<4, 4, BK, R2T, MODE>(grid, s, a);
+        else cg_launch<4, 8, BK, R2T, MODE>(grid, s, a);
     }
 }
-template <int BK, int R2, int MODE>
-void cg_wn(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    switch (WN) {
-        case 1: cg_mt<1, BK, R2, MODE>(MT, grid, s, a); break;
-        case 2: cg_mt<2, BK, R2, MODE>(MT, grid, s, a); break;
-        case 4: cg_mt<4, BK, R2, MODE>(MT, grid, s, a); break;
-        default: cg_mt<8, BK, R2, MODE>(MT, grid, s, a); break;
-    }
-}
-// BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16
+// BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16;
+// R2 = 2, 4 compiled in, anything else at run time
 template <int MODE>
 void cg_run(int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     const bool b28 = (K % 28) == 0;
     if (R2 == 2) {
-        if (b28) cg_wn<28, 2, MODE>(MT, WN, grid, s, a);
-        else cg_wn<16, 2, MODE>(MT, WN, grid, s, a);
+        if (b28) cg_tiles<28, 2, MODE>(MT, WN, grid, s, a);
+        else cg_tiles<16, 2, MODE>(MT, WN, grid, s, a);
+    } else if (R2 == 4) {
+        if (b28) cg_tiles<28, 4, MODE>(MT, WN, grid, s, a);
+        else cg_tiles<16, 4, MODE>(MT, WN, grid, s, a);
     } else {
-        if (b28) cg_wn<28, 4, MODE>(MT, WN, grid, s, a);
-        else cg_wn<16, 4, MODE>(MT, WN, grid, s, a);
+        if (b28) cg_tiles<28, 0, MODE>(MT, WN, grid, s, a);
+        else cg_tiles<16, 0, MODE>(MT, WN, grid, s, a);
     }
 }
-template <int MT, int WN, int BK, int R2>
-void cg_allow_one() {
-    const int lim = 200 * 1024;
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_LEAF_UP>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_LEAF_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_UPX>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_UPY>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2, CG_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+template <int MT, int WN, int BK, int R2T, int MODE>
+void cg_allow1() {
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
-template <int WN, int BK, int R2>
-void cg_allow_mt() { cg_allow_one<2, WN, BK, R2>(); cg_allow_one<4, WN, BK, R2>(); cg_allow_one<5, WN, BK, R2>(); }
-template <int BK, int R2>
-void cg_allow_wn() { cg_allow_mt<1, BK, R2>(); cg_allow_mt<2, BK, R2>(); cg_allow_mt<4, BK, R2>(); cg_allow_mt<8, BK, R2>(); }
-template <int R2>
-void cg_allow_r2() { cg_allow_wn<16, R2>(); cg_allow_wn<28, R2>(); }
+template <int BK, int R2T, int MODE>
+void cg_allow_mode() {
+    if (MODE == CG_LEAF_UP || MODE == CG_LEAF_DOWN) {
+        cg_allow1<4, 8, BK, R2T, MODE>(); cg_allow1<5, 8, BK, R2T, MODE>();
+        return;
+    }
+    cg_allow1<2, 2, BK, R2T, MODE>(); cg_allow1<2, 4, BK, R2T, MODE>(); cg_allow1<2, 8, BK, R2T, MODE>();
+    cg_allow1<4, 2, BK, R2T, MODE>(); cg_allow1<4, 4, BK, R2T, MODE>(); cg_allow1<4, 8, BK, R2T, MODE>();
+}
+template <int BK, int R2T>
+void cg_allow_bk() {
+    cg_allow_mode<BK, R2T, CG_LEAF_UP>(); cg_allow_mode<BK, R2T, CG_LEAF_DOWN>(); cg_allow_mode<BK, R2T, CG_UPX>();
+    cg_allow_mode<BK, R2T, CG_UPY>(); cg_allow_mode<BK, R2T, CG_DOWN>(); cg_allow_mode<BK, R2T, CG_ROOT>();
+}
+template <int R2T>
+void cg_allow_r2() { cg_allow_bk<16, R2T>(); cg_allow_bk<28, R2T>(); }
 
 // tile choice for a GEMM with `rows` output rows and `ncols` columns:
 // fewest padded rows, ties to the larger tile
-void cg_tile(int rows, int ncols, int& MT, int& WN) {
-    int best = 5, bestw = 1 << 30;
-    for (int mt : {5, 4, 2}) {
+void cg_tile(int rows, int ncols, int& MT, int& WN, bool leaf = false) {
+    int best = 4, bestw = 1 << 30;
+    const int cands_leaf[2] = {5, 4}, cands[2] = {4, 2};
+    for (int k = 0; k < 2; ++k) {
+        const int mt = leaf ? cands_leaf[k] : cands[k];
         const int bm = 8 * mt;
         const int waste = ((rows + bm - 1) / bm) * bm - rows;
         if (waste < bestw) { best = mt; bestw = waste; }
     }
     MT = best;
-    WN = ncols >= 64 ? 8 : ncols >= 32 ? 4 : ncols >= 16 ? 2 : 1;
+    WN = leaf ? 8 : (ncols >= 64 ? 8 : ncols >= 32 ? 4 : 2);
 }
 
 }  // namespace
 
 void DeviceStore::configure_kernels() {
+    cg_allow_r2<0>();
     cudaFuncSetAttribute(k_leaf_fdm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_fdm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_fdm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1072,7 +1117,11 @@ void DeviceStore::configure_kernels() {
     allow_all<8>();
 }
 
-int DeviceStore::launches_per_step() const { return (shared && R2 <= 4 && !fdm ? 7 : 6) + 3 * static_cast<int>(levels.size()); }
+int DeviceStore::launches_per_step() const {
+    const int nchunks = (nh + chunk - 1) / chunk;
+    const int per_chunk = (shared && !fdm ? 5 : 4) + 3 * static_cast<int>(levels.size());
+    return 2 + nchunks * per_chunk;
+}
 
 int DeviceStore::check(const char* what) {
     const cudaError_t e = cudaGetLastError();
@@ -1084,57 +1133,51 @@ int DeviceStore::check(const char* what) {
 }
 
 // Solve all half poles of this handle for the state in d_state (up to leaf_down).
-int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
-    // pre
-    {
-        PreArgs a{};
-        a.u = d_state; a.F = d_F; a.elem_g = d_elem_g; a.D = d_D; a.kappa = d_kappa;
-        a.model = model; a.n = n; a.p = p; a.q = q; a.R2 = R2; a.nF = nF; a.N = N; a.NI = NI; a.c1 = c1;
-        const long long tot = NI * R2;
-        tbeg(s);
-        k_pre<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
-        tend(T_PRE, s);
-    }
-    // GEMM path: shared store, nrhs <= 2 (DMMA complex GEMM over all nodes of a level)
-    const bool gemm = shared && R2 <= 4;
-    const int NBl = pick_nb(nelem, R2, shared);
+// leaf solves and merge sweeps for local half poles [m0, m0 + pc) (work buffers are chunk-local)
+int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
+    const double2* cF = d_cF + static_cast<size_t>(m0) * nF;
     const int thr = ((q2 + 31) / 32) * 32;
+    const int NBl = pick_nb(nelem, R2, shared);
+    // ---- leaves up ----
     FdmArgs fd{};
     if (fdm) {
-        fd.V = d_V; fd.Vinv = d_Vinv; fd.Dinv = d_Dinv; fd.D = d_D; fd.D2 = d_D2; fd.F = d_F; fd.cF = d_cF;
-        fd.q = q; fd.p = p; fd.nF = nF; fd.nelem = nelem; fd.R2 = R2; fd.nh = nh; fd.c1 = c1; fd.c2 = c1 * c1;
+        fd.V = d_V; fd.Vinv = d_Vinv; fd.Dinv = d_Dinv + static_cast<size_t>(m0) * FDM_T * FDM_T;
+        fd.D = d_D; fd.D2 = d_D2; fd.F = d_F; fd.cF = cF;
+        fd.q = q; fd.p = p; fd.nF = nF; fd.nelem = nelem; fd.R2 = R2; fd.nh = pc; fd.c1 = c1; fd.c2 = c1 * c1;
         fd.h = d_h[0]; fd.hps = hstride; fd.edge = d_edge; fd.NE = NE; fd.gB = d_leaf_gB; fd.w = d_w;
-        fd.dE = d_dE; fd.nE = nE; fd.pgroup = pgroup; fd.ngroups = ngroups; fd.Epart = d_Epart;
+        fd.dE = d_dE + static_cast<size_t>(m0) * nE; fd.nE = nE; fd.pgroup = pgroup; fd.ngroups = ngroups;
+        fd.Epart = d_Epart;
     }
-    const long long nprob = static_cast<long long>(nh) * nelem * R2;
+    const long long nprob = static_cast<long long>(pc) * nelem * R2;
     const unsigned fdm_blocks = static_cast<unsigned>((nprob + FDM_WARPS - 1) / FDM_WARPS);
     const size_t fdm_smem = (static_cast<size_t>(FDM_WARPS) * FDM_TILE_ELEMS + FDM_T * FDM_LDV) * sizeof(double2);
     if (fdm) {
         tbeg(s);
         k_leaf_fdm<0><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
         tend(T_LEAF_UP, s);
-    } else if (gemm) {
+    } else if (shared) {
         CgemmArgs a{};
-        a.A = d_Ainv; a.rows = q2; a.K = q2; a.nodes = nelem;
-        a.F = d_F; a.cF = d_cF; a.nF = nF; a.q2 = q2; a.dst = d_w;
+        a.A = d_Ainv + static_cast<size_t>(m0) * pp_Ainv; a.rows = q2; a.K = q2; a.nodes = nelem; a.R2 = R2;
+        a.F = d_F; a.cF = cF; a.nF = nF; a.q2 = q2; a.dst = d_w;
         int MT, WN;
-        cg_tile(q2, nelem * R2, MT, WN);
+        cg_tile(q2, nelem * R2, MT, WN, true);
         a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
         const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
         tbeg(s);
-        cg_run<CG_LEAF_UP>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
+        cg_run<CG_LEAF_UP>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
         tend(T_LEAF_UP, s);
         FluxArgs fa{};
         fa.w = d_w; fa.h = d_h[0]; fa.D = d_D; fa.c1 = c1; fa.hps = hstride; fa.q = q; fa.nelem = nelem; fa.R2 = R2;
         tbeg(s);
-        k_leaf_flux<<<dim3((nelem + FLUX_LB - 1) / FLUX_LB, nh), 256,
+        k_leaf_flux<<<dim3((nelem + FLUX_LB - 1) / FLUX_LB, pc), 256,
                       static_cast<size_t>(FLUX_LB) * q2 * R2 * sizeof(double2), s>>>(fa);
         tend(T_LEAF_FLUX, s);
     } else {
         LeafUpArgs a{};
-        a.Ainv = d_Ainv; a.F = d_F; a.cF = d_cF; a.D = d_D; a.c1 = c1; a.w = d_w; a.h = d_h[0]; a.hps = hstride;
-        a.q = q; a.q2 = q2; a.nb = nb; a.nF = nF; a.nelem = nelem; a.shared = shared ? 1 : 0;
-        dim3 grid(nelem / NBl, nh);
+        a.Ainv = d_Ainv + static_cast<size_t>(m0) * pp_Ainv; a.F = d_F; a.cF = cF; a.D = d_D; a.c1 = c1; a.w = d_w;
+        a.h = d_h[0]; a.hps = hstride;
+        a.q = q; a.q2 = q2; a.nb = nb; a.nF = nF; a.nelem = nelem; a.shared = 0;
+        dim3 grid(nelem / NBl, pc);
         const size_t smem = static_cast<size_t>(NBl) * q2 * R2 * sizeof(double2);
         tbeg(s);
         switch (R2) {
@@ -1144,36 +1187,37 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         }
         tend(T_LEAF_UP, s);
     }
-    // merges up
+    // ---- merges up ----
     for (size_t li = 0; li < levels.size(); ++li) {
         Level& L = levels[li];
         const double2* hc = d_h[li % 2];
         double2* hp = d_h[(li + 1) % 2];
-        const bool lg = gemm && L.nodes * R2 >= 4;
-        if (lg) {
+        const double2* X = L.X + static_cast<size_t>(m0) * L.ppX;
+        const double2* Y = L.Y + static_cast<size_t>(m0) * L.ppY;
+        if (shared && L.nodes * R2 >= 4) {
             int MT, WN;
             {  // X stage: w3 = Xneg (h^a_3 + h^b_3)
                 CgemmArgs a{};
-                a.A = L.X; a.rows = L.n3; a.K = L.n3; a.nodes = L.nodes;
+                a.A = X; a.rows = L.n3; a.K = L.n3; a.nodes = L.nodes; a.R2 = R2;
                 a.src = hc; a.src_ps = hstride; a.bi0 = L.ia3; a.bi1 = L.ib3;
                 a.dst = L.w3; a.dst_ps = static_cast<long long>(L.nodes) * L.n3;
                 cg_tile(L.n3, L.nodes * R2, MT, WN);
                 a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
                 const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
                 tbeg(s);
-                cg_run<CG_UPX>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
+                cg_run<CG_UPX>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
                 tend(T_MERGE_UP, s);
             }
             {  // Y stage: h = h_child[ext] + Y w3
                 CgemmArgs a{};
-                a.A = L.Y; a.rows = L.next; a.K = L.n3; a.nodes = L.nodes;
+                a.A = Y; a.rows = L.next; a.K = L.n3; a.nodes = L.nodes; a.R2 = R2;
                 a.src = L.w3; a.src_ps = static_cast<long long>(L.nodes) * L.n3;
                 a.dst = hp; a.dst_ps = hstride; a.add = hc; a.add_ps = hstride; a.ai0 = L.ext;
                 cg_tile(L.next, L.nodes * R2, MT, WN);
                 a.nrowblk = (L.next + 8 * MT - 1) / (8 * MT);
                 const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
                 tbeg(s);
-                cg_run<CG_UPY>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
+                cg_run<CG_UPY>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
                 tend(T_MERGE_UP, s);
             }
             continue;
@@ -1181,42 +1225,58 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         const int NB = pick_nb(L.nodes, R2, shared);
         {  // X stage
             GemvArgs g = gemv_shape(L.n3, L.n3, L.nodes, shared);
-            g.M = L.X; g.xsrc = hc; g.xsrc_ps = hstride; g.xi0 = L.ia3; g.xi1 = L.ib3;
+            g.M = X; g.xsrc = hc; g.xsrc_ps = hstride; g.xi0 = L.ia3; g.xi1 = L.ib3;
             g.ydst = L.w3; g.ydst_ps = static_cast<long long>(L.nodes) * L.n3;
-            dim3 grid((L.nodes / NB) * g.nrowblk, nh);
+            dim3 grid((L.nodes / NB) * g.nrowblk, pc);
             tbeg(s);
             launch_gemv<MODE_UPX>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
             tend(T_MERGE_UP, s);
         }
         {  // Y stage
             GemvArgs g = gemv_shape(L.next, L.n3, L.nodes, shared);
-            g.M = L.Y; g.xsrc = L.w3; g.xsrc_ps = static_cast<long long>(L.nodes) * L.n3;
+            g.M = Y; g.xsrc = L.w3; g.xsrc_ps = static_cast<long long>(L.nodes) * L.n3;
             g.ysrc = hc; g.ysrc_ps = hstride; g.yi = L.ext;
             g.ydst = hp; g.ydst_ps = hstride;
-            dim3 grid((L.nodes / NB) * g.nrowblk, nh);
+            dim3 grid((L.nodes / NB) * g.nrowblk, pc);
             tbeg(s);
             launch_gemv<MODE_UPY>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
             tend(T_MERGE_UP, s);
         }
     }
-    // root closure
+    // ---- periodic closure ----
     {
         const double2* hr = d_h[levels.size() % 2];
-        GemvArgs g = gemv_shape(ns, ns, 1, true);
-        g.shared = 1;
-        g.M = d_Xroot; g.xsrc = hr; g.xsrc_ps = hstride; g.xi0 = d_rpos1; g.xi1 = d_rpos2;
-        g.ydst = d_edge; g.ydst_ps = NE; g.yo = d_rgs;
-        dim3 grid(g.nrowblk, nh);
-        tbeg(s);
-        launch_gemv<MODE_ROOT>(R2, 1, grid, gemv_smem(g, 1, R2), s, g);
-        tend(T_ROOT, s);
+        const double2* Xr = d_Xroot + static_cast<size_t>(m0) * pp_Xroot;
+        if (shared && R2 > 2) {
+            CgemmArgs a{};
+            a.A = Xr; a.rows = ns; a.K = ns; a.nodes = 1; a.R2 = R2;
+            a.src = hr; a.src_ps = hstride; a.bi0 = d_rpos1; a.bi1 = d_rpos2;
+            a.dst = d_edge; a.dst_ps = NE; a.so0 = d_rgs;
+            int MT, WN;
+            cg_tile(ns, R2, MT, WN);
+            a.nrowblk = (ns + 8 * MT - 1) / (8 * MT);
+            const int ncb = (R2 + 8 * WN - 1) / (8 * WN);
+            tbeg(s);
+            cg_run<CG_ROOT>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
+            tend(T_ROOT, s);
+        } else {
+            GemvArgs g = gemv_shape(ns, ns, 1, true);
+            g.shared = 1;
+            g.M = Xr; g.xsrc = hr; g.xsrc_ps = hstride; g.xi0 = d_rpos1; g.xi1 = d_rpos2;
+            g.ydst = d_edge; g.ydst_ps = NE; g.yo = d_rgs;
+            dim3 grid(g.nrowblk, pc);
+            tbeg(s);
+            launch_gemv<MODE_ROOT>(R2, 1, grid, gemv_smem(g, 1, R2), s, g);
+            tend(T_ROOT, s);
+        }
     }
-    // merges down
+    // ---- merges down ----
     for (int li = static_cast<int>(levels.size()) - 1; li >= 0; --li) {
         Level& L = levels[li];
-        if (gemm && L.nodes * R2 >= 4) {
+        const double2* S = L.S + static_cast<size_t>(m0) * L.ppS;
+        if (shared && L.nodes * R2 >= 4) {
             CgemmArgs a{};
-            a.A = L.S; a.rows = L.n3; a.K = L.next; a.nodes = L.nodes;
+            a.A = S; a.rows = L.n3; a.K = L.next; a.nodes = L.nodes; a.R2 = R2;
             a.src = d_edge; a.src_ps = NE; a.bi0 = L.gext;
             a.add = L.w3; a.add_ps = static_cast<long long>(L.nodes) * L.n3;
             a.dst = d_edge; a.dst_ps = NE; a.so0 = L.g3;
@@ -1225,21 +1285,21 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
             a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
             const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
             tbeg(s);
-            cg_run<CG_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
+            cg_run<CG_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
             tend(T_MERGE_DOWN, s);
             continue;
         }
         const int NB = pick_nb(L.nodes, R2, shared);
         GemvArgs g = gemv_shape(L.n3, L.next, L.nodes, shared);
-        g.M = L.S; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
+        g.M = S; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
         g.ysrc = L.w3; g.ysrc_ps = static_cast<long long>(L.nodes) * L.n3;
         g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
-        dim3 grid((L.nodes / NB) * g.nrowblk, nh);
+        dim3 grid((L.nodes / NB) * g.nrowblk, pc);
         tbeg(s);
         launch_gemv<MODE_DOWN>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
         tend(T_MERGE_DOWN, s);
     }
-    // leaves down
+    // ---- leaves down ----
     if (fdm && fuse_sum) {
         // downward leaf solves fused with the interior pole sums (u_m stays on chip)
         const long long nsum = static_cast<long long>(ngroups) * nelem * R2;
@@ -1250,22 +1310,22 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         tbeg(s);
         k_leaf_fdm<1><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
         tend(T_LEAF_DOWN, s);
-    } else if (gemm) {
+    } else if (shared) {
         CgemmArgs a{};
-        a.A = d_Sleaf; a.rows = q2; a.K = nb; a.nodes = nelem;
+        a.A = d_Sleaf + static_cast<size_t>(m0) * pp_Sleaf; a.rows = q2; a.K = nb; a.nodes = nelem; a.R2 = R2;
         a.src = d_edge; a.src_ps = NE; a.bi0 = d_leaf_gB; a.dst = d_w;
         int MT, WN;
-        cg_tile(q2, nelem * R2, MT, WN);
+        cg_tile(q2, nelem * R2, MT, WN, true);
         a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
         const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
         tbeg(s);
-        cg_run<CG_LEAF_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, nh), s, a);
+        cg_run<CG_LEAF_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
         tend(T_LEAF_DOWN, s);
     } else {
         LeafDownArgs a{};
-        a.S = d_Sleaf; a.edge = d_edge; a.gB = d_leaf_gB; a.w = d_w; a.NE = NE;
-        a.q2 = q2; a.nb = nb; a.nelem = nelem; a.shared = shared ? 1 : 0;
-        dim3 grid(nelem / NBl, nh);
+        a.S = d_Sleaf + static_cast<size_t>(m0) * pp_Sleaf; a.edge = d_edge; a.gB = d_leaf_gB; a.w = d_w; a.NE = NE;
+        a.q2 = q2; a.nb = nb; a.nelem = nelem; a.shared = 0;
+        dim3 grid(nelem / NBl, pc);
         const size_t smem = static_cast<size_t>(NBl) * nb * R2 * sizeof(double2);
         tbeg(s);
         switch (R2) {
@@ -1275,14 +1335,14 @@ int DeviceStore::solve_poles(const double* d_state, cudaStream_t s) {
         }
         tend(T_LEAF_DOWN, s);
     }
-    return check("solve_poles");
+    return check("tree_chunk");
 }
 
-int DeviceStore::pole_sum(double* d_E_out, cudaStream_t s) {
-    if (fdm && fuse_sum) {
+int DeviceStore::pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s) {
+    if (fuse_sum) {
         PoleSum2Args a{};
         a.Epart = d_Epart; a.edge = d_edge; a.dE = d_dE; a.E = d_E_out;
-        a.N = N; a.NI = NI; a.NE = NE; a.nh = nh; a.nE = nE; a.R2 = R2; a.ngroups = ngroups;
+        a.N = N; a.NI = NI; a.NE = NE; a.nh = pc; a.nE = nE; a.R2 = R2; a.ngroups = ngroups;
         const long long tot = N * R2;
         tbeg(s);
         k_pole_sum_fused<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
@@ -1290,13 +1350,33 @@ int DeviceStore::pole_sum(double* d_E_out, cudaStream_t s) {
         return check("pole_sum");
     }
     PoleSumArgs a{};
-    a.w = d_w; a.edge = d_edge; a.dE = d_dE; a.E = d_E_out;
-    a.N = N; a.NI = NI; a.NE = NE; a.nh = nh; a.nE = nE; a.R2 = R2;
+    a.accumulate = accumulate ? 1 : 0;
+    a.w = d_w; a.edge = d_edge; a.dE = d_dE + static_cast<size_t>(m0) * nE; a.E = d_E_out;
+    a.N = N; a.NI = NI; a.NE = NE; a.nh = pc; a.nE = nE; a.R2 = R2;
     const long long tot = N * R2;
     tbeg(s);
     k_pole_sum<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
     tend(T_POLE_SUM, s);
     return check("pole_sum");
+}
+
+int DeviceStore::solve_sum(const double* d_state, double* d_E_out, cudaStream_t s) {
+    {
+        PreArgs a{};
+        a.u = d_state; a.F = d_F; a.elem_g = d_elem_g; a.D = d_D; a.kappa = d_kappa;
+        a.model = model; a.n = n; a.p = p; a.q = q; a.R2 = R2; a.nF = nF; a.N = N; a.NI = NI; a.c1 = c1;
+        const long long tot = NI * R2;
+        tbeg(s);
+        k_pre<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
+        tend(T_PRE, s);
+    }
+    int rc;
+    for (int m0 = 0; m0 < nh; m0 += chunk) {
+        const int pc = std::min(chunk, nh - m0);
+        if ((rc = tree_chunk(m0, pc, s))) return rc;
+        if ((rc = pole_sum_chunk(m0, pc, m0 > 0, d_E_out, s))) return rc;
+    }
+    return REXP_OK;
 }
 
 int DeviceStore::recover(const double* d_E_in, double* d_state, cudaStream_t s) {
@@ -1313,9 +1393,8 @@ int DeviceStore::recover(const double* d_E_in, double* d_state, cudaStream_t s) 
 }
 
 int DeviceStore::step(double* d_state, cudaStream_t s) {
-    int rc = solve_poles(d_state, s);
+    int rc = solve_sum(d_state, d_E, s);
     if (rc) return rc;
-    if ((rc = pole_sum(d_E, s))) return rc;
     return recover(d_E, d_state, s);
 }
 

@@ -14,19 +14,21 @@ struct Level {
     int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0;
     double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
     int *ia3 = nullptr, *ib3 = nullptr, *ext = nullptr, *gext = nullptr, *g3 = nullptr;
-    double2* w3 = nullptr;                              // [nh][nodes][n3][R2]
+    double2* w3 = nullptr;                              // [chunk][nodes][n3][R2]
+    size_t ppX = 0, ppY = 0, ppS = 0;                   // per-pole operator sizes (complex)
 };
 
 class DeviceStore {
   public:
     ~DeviceStore();
-    int init(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1, bool shared, int nrhs,
-             const std::vector<HostLevelOps>& ops);
+    int init(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1, bool shared, int nrhs);
+    int upload_ops(const std::vector<HostLevelOps>& ops, int m0);
     void release();
     // one full step on a device state [nrhs][3][N] complex128
     int step(double* d_state, cudaStream_t s);
-    int solve_poles(const double* d_state, cudaStream_t s);
-    int pole_sum(double* d_E_out, cudaStream_t s);
+    // all half poles of the handle, chunk by chunk: leaf solves, merge sweeps and
+    // the weighted pole sums E (written to d_E_out)
+    int solve_sum(const double* d_state, double* d_E_out, cudaStream_t s);
     int recover(const double* d_E_in, double* d_state, cudaStream_t s);
     int launches_per_step() const;
 
@@ -71,6 +73,10 @@ class DeviceStore {
     double2 *d_cF = nullptr, *d_dE = nullptr, *d_Dinv = nullptr;
     double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_Epart = nullptr;
     int pgroup = 1, ngroups = 1;
+    int chunk = 1;             // half poles per work-buffer chunk
+    size_t pp_Ainv = 0, pp_Sleaf = 0, pp_Xroot = 0;
+    int tree_chunk(int m0, int pc, cudaStream_t s);
+    int pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s);
     double2 *d_Ainv = nullptr, *d_Sleaf = nullptr, *d_Xroot = nullptr;
     double2 *d_w = nullptr, *d_edge = nullptr;
     double2* d_h[2] = {nullptr, nullptr};

@@ -87,6 +87,23 @@ def test_config0_nrhs2_and_host_path(c0):
     h.close()
 
 
+@pytest.mark.parametrize("nrhs,chunk", [(8, "37"), (3, "1000")])
+def test_config0_many_rhs_and_pole_chunks(c0, nrhs, chunk, monkeypatch):
+    """Multi-RHS path (config 3's shape at config 0 size): nrhs independent states,
+    runtime-R2 DMMA GEMMs at every level incl. the periodic closure, and the pole
+    sums accumulated over chunks of half poles (REXP_CHUNK)."""
+    cfg, m, op, u0 = c0
+    Lam = cfg["Lambda_tau"] / cfg["tau"]
+    monkeypatch.setenv("REXP_CHUNK", chunk)
+    U = np.stack([rsw_initial_state(m.x, m.y, cfg["seed"] + 10 * k) for k in range(nrhs)])
+    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], nrhs=nrhs)
+    got = _gpu_apply(h, U, 2)
+    errs = [rel_l2(got[k], op.evolve(U[k], 2)) for k in range(nrhs)]
+    print(f"nrhs {nrhs} chunk {chunk}: max rel L2 {max(errs):.3e}")
+    assert max(errs) <= TOL
+    h.close()
+
+
 def test_edge_cases_zero_state_and_zero_steps(c0):
     cfg, m, op, u0 = c0
     Lam = cfg["Lambda_tau"] / cfg["tau"]
