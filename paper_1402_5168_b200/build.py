@@ -20,32 +20,41 @@ GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def _run(cmd):
-    print(" ".join(cmd), flush=True)
+    print(" ".join(cmd[:2] + ["..."] + cmd[-3:]), flush=True)
     subprocess.check_call(cmd)
 
 
 def build(force=False, verbose_ptxas=False):
+    """Compile every translation unit (in parallel) and link librexp.so."""
+    import concurrent.futures as cf
     os.makedirs(BUILD, exist_ok=True)
-    srcs = [os.path.join(CSRC, f) for f in CU + CPP] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".h"))]
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     srcs.append(os.path.join(os.path.dirname(HERE), "include", "rexp.h"))
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(s) <= t for s in srcs):
             return LIB
-    objs = []
+    jobs = []
     for f in CU:
         o = os.path.join(BUILD, f + ".o")
         cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c",
                os.path.join(CSRC, f), "-o", o]
         if verbose_ptxas:
             cmd.insert(1, "-Xptxas=-v")
-        _run(cmd)
-        objs.append(o)
+        jobs.append((cmd, o))
+    for mode in range(6):   # k_cgemm tile instantiations, one object per mode
+        o = os.path.join(BUILD, f"cgemm_mode{mode}.o")
+        jobs.append(([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-DCG_MODE={mode}",
+                      "-c", os.path.join(CSRC, "cgemm_mode.cu"), "-o", o], o))
     for f in CPP:
         o = os.path.join(BUILD, f + ".o")
-        _run(["g++", "-O3", "-mavx2", "-mfma", "-std=c++17", "-fPIC", "-Wall", "-I", os.path.join(CUDA, "include"),
-              "-c", os.path.join(CSRC, f), "-o", o])
-        objs.append(o)
+        jobs.append((["g++", "-O3", "-mavx2", "-mfma", "-std=c++17", "-fPIC", "-Wall", "-I",
+                      os.path.join(CUDA, "include"), "-c", os.path.join(CSRC, f), "-o", o], o))
+    with cf.ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        futs = [ex.submit(_run, cmd) for cmd, _ in jobs]
+        for fu in futs:
+            fu.result()
+    objs = [o for _, o in jobs]
     _run([NVCC, *GENCODE, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"])
     return LIB
 

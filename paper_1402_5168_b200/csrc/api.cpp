@@ -122,8 +122,8 @@ int rexp_setup(const rexp_problem* prob, double tau, double delta, double Lambda
     h->shared = store == REXP_STORE_SHARED;
     h->nrhs = opt.nrhs;
     h->device = opt.device;
-    if (!h->shared && opt.nrhs > 4) {
-        set_error("rexp_setup: the per-node store supports nrhs <= 4");
+    if (!h->shared && opt.nrhs != 1 && opt.nrhs != 2 && opt.nrhs != 4) {
+        set_error("rexp_setup: the per-node store supports nrhs = 1, 2 or 4");
         return REXP_EINVAL;
     }
     if (opt.device < 0) {

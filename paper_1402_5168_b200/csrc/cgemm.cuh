@@ -119,15 +119,15 @@ __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int
     }
 }
 
-template <int MT, int WN, int BK, int NTW = 1>
+template <int MT, int WN, int BK, int NTW = 1, int WM = 1>
 constexpr size_t cgemm_smem_bytes() {
-    return 2 * (size_t)BK * ((8 * MT + 2) + (8 * WN * NTW + 2)) * sizeof(double2);
+    return 2 * (size_t)BK * ((8 * MT * WM + 2) + (8 * WN * NTW + 2)) * sizeof(double2);
 }
 
-// MT m-tiles and NTW n-tiles per warp; WN warps side by side in n.
-template <int MT, int WN, int BK, int R2T, int MODE, int NTW = 1, int MINB = 1>
-__global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
-    constexpr int BM = 8 * MT, BN = 8 * WN * NTW, NT = 32 * WN;
+// MT m-tiles and NTW n-tiles per warp; WN warps side by side in n, WM in m.
+template <int MT, int WN, int BK, int R2T, int MODE, int NTW = 1, int MINB = 1, int WM = 1>
+__global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
+    constexpr int BM = 8 * MT * WM, BN = 8 * WN * NTW, NT = 32 * WN * WM;
     const int R2 = R2T ? R2T : a.R2;
     static_assert(BK % 4 == 0, "BK must be a multiple of the DMMA k (4)");
     constexpr int LDA = BM + 2, LDB = BN + 2;
@@ -139,8 +139,10 @@ __global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
     const int cb = blockIdx.x / a.nrowblk;
     const int row0 = rb * BM, col0 = cb * BN;
     const int ncols = a.nodes * R2;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int warp = wid % WN, wm = wid / WN;          // n position, m position of this warp
     const int g = lane >> 2, t4 = lane & 3;
+    const int mrow0 = wm * MT * 8;                     // first row of this warp inside the CTA tile
     const double2* Am = a.A + (size_t)m * a.rows * a.K;
     double2 cf[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
     if (MODE == CG_LEAF_UP) {
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
             for (int n = 0; n < NTW; ++n)
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
-                    const int row = row0 + i * 8 + g;
+                    const int row = row0 + mrow0 + i * 8 + g;
                     const int col = col0 + (warp * NTW + n) * 8 + 2 * t4 + j;
                     addv[i][n][j] = make_double2(0.0, 0.0);
                     if (row < a.rows && col < ncols) {
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
             for (int n = 0; n < NTW; ++n) b[n] = Bb[kk * LDB + (warp * NTW + n) * 8 + g];   // B[k = t4][n = g]
             double2 av[MT];
 #pragma unroll
-            for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + i * 8 + g];   // A[m = g][k = t4]
+            for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + mrow0 + i * 8 + g];   // A[m = g][k = t4]
             // four passes so each accumulator is revisited only every 2*MT*NTW DMMAs
 #pragma unroll
             for (int n = 0; n < NTW; ++n)
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(32 * WN, MINB) k_cgemm(CgemmArgs a) {
     // epilogue: C[g][2 t4 + j] of each tile
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
-        const int row = row0 + i * 8 + g;
+        const int row = row0 + mrow0 + i * 8 + g;
         if (row >= a.rows) continue;
 #pragma unroll
         for (int n = 0; n < NTW; ++n)

@@ -26,6 +26,7 @@
 
 #include "rexp_device.hpp"
 #include "cgemm.cuh"
+#include "cgemm_launch.hpp"
 #include "leaf_fdm.cuh"
 
 namespace rexp {
@@ -771,8 +772,8 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     c1 = 2.0 * n;
     scal = pt.scal;
     int rc;
-    if (!shared && R2 > 8) {
-        set_error("the per-node store supports nrhs <= 4");
+    if (!shared && R2 != 2 && R2 != 4 && R2 != 8) {
+        set_error("the per-node store supports nrhs = 1, 2 or 4");
         return REXP_EINVAL;
     }
     // mesh data
@@ -913,8 +914,13 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     }
     if ((rc = walloc(&d_E, static_cast<size_t>(nE) * R2 * N, 8))) return rc;
     if ((rc = walloc(&d_u, static_cast<size_t>(nrhs) * 3 * N * 2, 8))) return rc;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     configure_kernels();
-    return REXP_OK;
+    return tune_stages();
 }
 
 // copy the host factorization of local half poles [m0, m0 + count) into the store
@@ -1028,90 +1034,30 @@ size_t gemv_smem(const GemvArgs& g, int NB, int R2) {
 }
 
 
-template <int MT, int WN, int BK, int R2T, int MODE>
-void cg_launch(dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    k_cgemm<MT, WN, BK, R2T, MODE><<<grid, 32 * WN, cgemm_smem_bytes<MT, WN, BK>(), s>>>(a);
-}
-// merge-level tiles: MT in {2, 4}, WN in {2, 4, 8}; leaf tiles: MT in {4, 5}, WN = 8
-template <int BK, int R2T, int MODE>
-void cg_tiles(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    if (MODE == CG_LEAF_UP || MODE == CG_LEAF_DOWN) {
-        if (MT == 4) cg_launch<4, 8, BK, R2T, MODE>(grid, s, a);
-        else cg_launch<5, 8, BK, R2T, MODE>(grid, s, a);
-        return;
-    }
-    if (MT == 2) {
-        if (WN == 2) cg_launch<2, 2, BK, R2T, MODE>(grid, s, a);
-        else if (WN == 4) cg_launch<2, 4, BK, R2T, MODE>(grid, s, a);
-        else cg_launch<2, 8, BK, R2T, MODE>(grid, s, a);
-    } else {
-        if (WN == 2) cg_launch<4, 2, BK, R2T, MODE>(grid, s, a);
-        else if (WN == 4) cg_launch<4, 4, BK, R2T, MODE>(grid, s, a);
-        else cg_launch<4, 8, BK, R2T, MODE>(grid, s, a);
-    }
-}
-// BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16;
-// R2 = 2, 4 compiled in, anything else at run time
-template <int MODE>
-void cg_run(int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    const bool b28 = (K % 28) == 0;
-    if (R2 == 2) {
-        if (b28) cg_tiles<28, 2, MODE>(MT, WN, grid, s, a);
-        else cg_tiles<16, 2, MODE>(MT, WN, grid, s, a);
-    } else if (R2 == 4) {
-        if (b28) cg_tiles<28, 4, MODE>(MT, WN, grid, s, a);
-        else cg_tiles<16, 4, MODE>(MT, WN, grid, s, a);
-    } else {
-        if (b28) cg_tiles<28, 0, MODE>(MT, WN, grid, s, a);
-        else cg_tiles<16, 0, MODE>(MT, WN, grid, s, a);
-    }
-}
-template <int MT, int WN, int BK, int R2T, int MODE>
-void cg_allow1() {
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-}
-template <int BK, int R2T, int MODE>
-void cg_allow_mode() {
-    if (MODE == CG_LEAF_UP || MODE == CG_LEAF_DOWN) {
-        cg_allow1<4, 8, BK, R2T, MODE>(); cg_allow1<5, 8, BK, R2T, MODE>();
-        return;
-    }
-    cg_allow1<2, 2, BK, R2T, MODE>(); cg_allow1<2, 4, BK, R2T, MODE>(); cg_allow1<2, 8, BK, R2T, MODE>();
-    cg_allow1<4, 2, BK, R2T, MODE>(); cg_allow1<4, 4, BK, R2T, MODE>(); cg_allow1<4, 8, BK, R2T, MODE>();
-}
-template <int BK, int R2T>
-void cg_allow_bk() {
-    cg_allow_mode<BK, R2T, CG_LEAF_UP>(); cg_allow_mode<BK, R2T, CG_LEAF_DOWN>(); cg_allow_mode<BK, R2T, CG_UPX>();
-    cg_allow_mode<BK, R2T, CG_UPY>(); cg_allow_mode<BK, R2T, CG_DOWN>(); cg_allow_mode<BK, R2T, CG_ROOT>();
-}
-template <int R2T>
-void cg_allow_r2() { cg_allow_bk<16, R2T>(); cg_allow_bk<28, R2T>(); }
-
 // tile choice for a GEMM with `rows` output rows and `ncols` columns:
 // fewest padded rows, ties to the larger tile
 void cg_tile(int rows, int ncols, int& MT, int& WN, bool leaf = false) {
+    WN = leaf ? 8 : (ncols >= 64 ? 8 : ncols >= 32 ? 4 : 2);
+    const int wm = leaf ? 1 : cg_wm(WN);
     int best = 4, bestw = 1 << 30;
     const int cands_leaf[2] = {5, 4}, cands[2] = {4, 2};
     for (int k = 0; k < 2; ++k) {
         const int mt = leaf ? cands_leaf[k] : cands[k];
-        const int bm = 8 * mt;
+        const int bm = 8 * mt * wm;
         const int waste = ((rows + bm - 1) / bm) * bm - rows;
         if (waste < bestw) { best = mt; bestw = waste; }
     }
     MT = best;
-    WN = leaf ? 8 : (ncols >= 64 ? 8 : ncols >= 32 ? 4 : 2);
 }
 
 }  // namespace
 
 void DeviceStore::configure_kernels() {
-    cg_allow_r2<0>();
+    cg_allow_all();
     cudaFuncSetAttribute(k_leaf_fdm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_fdm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_fdm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cg_allow_r2<2>();
-    cg_allow_r2<4>();
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
@@ -1133,6 +1079,170 @@ int DeviceStore::check(const char* what) {
 }
 
 // Solve all half poles of this handle for the state in d_state (up to leaf_down).
+// One merge-tree stage for local half poles [m0, m0 + pc):
+//   kind 0 = X (w3 = -X (h^a_3 + h^b_3)), 1 = Y (h = h_child[ext] + Y w3),
+//   2 = DOWN (u3 = S u_ext + w3), 3 = periodic closure (level index ignored)
+// with either the DMMA GEMM (cfg.kind 0, tile cfg.MT x cfg.WN) or the GEMV kernel.
+int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, int pc, cudaStream_t s) {
+    if (kind == 3) {
+        const double2* hr = d_h[levels.size() % 2];
+        const double2* Xr = d_Xroot + static_cast<size_t>(m0) * pp_Xroot;
+        if (cfg.kind == 0) {
+            CgemmArgs a{};
+            a.A = Xr; a.rows = ns; a.K = ns; a.nodes = 1; a.R2 = R2;
+            a.src = hr; a.src_ps = hstride; a.bi0 = d_rpos1; a.bi1 = d_rpos2;
+            a.dst = d_edge; a.dst_ps = NE; a.so0 = d_rgs;
+            a.nrowblk = (ns + 8 * cfg.MT * cg_wm(cfg.WN) - 1) / (8 * cfg.MT * cg_wm(cfg.WN));
+            const int ncb = (R2 + 8 * cfg.WN - 1) / (8 * cfg.WN);
+            tbeg(s);
+            cg_run_mode(CG_ROOT, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
+            tend(T_ROOT, s);
+        } else {
+            GemvArgs g = gemv_shape(ns, ns, 1, true);
+            g.shared = 1;
+            g.M = Xr; g.xsrc = hr; g.xsrc_ps = hstride; g.xi0 = d_rpos1; g.xi1 = d_rpos2;
+            g.ydst = d_edge; g.ydst_ps = NE; g.yo = d_rgs;
+            tbeg(s);
+            launch_gemv<MODE_ROOT>(R2, 1, dim3(g.nrowblk, pc), gemv_smem(g, 1, R2), s, g);
+            tend(T_ROOT, s);
+        }
+        return REXP_OK;
+    }
+    Level& L = levels[li];
+    const double2* hc = d_h[li % 2];
+    double2* hp = d_h[(li + 1) % 2];
+    const int cls = kind == 2 ? T_MERGE_DOWN : T_MERGE_UP;
+    if (cfg.kind == 0) {
+        CgemmArgs a{};
+        a.nodes = L.nodes; a.R2 = R2;
+        int mode;
+        if (kind == 0) {
+            mode = CG_UPX;
+            a.A = L.X + static_cast<size_t>(m0) * L.ppX; a.rows = L.n3; a.K = L.n3;
+            a.src = hc; a.src_ps = hstride; a.bi0 = L.ia3; a.bi1 = L.ib3;
+            a.dst = L.w3; a.dst_ps = static_cast<long long>(L.nodes) * L.n3;
+        } else if (kind == 1) {
+            mode = CG_UPY;
+            a.A = L.Y + static_cast<size_t>(m0) * L.ppY; a.rows = L.next; a.K = L.n3;
+            a.src = L.w3; a.src_ps = static_cast<long long>(L.nodes) * L.n3;
+            a.dst = hp; a.dst_ps = hstride; a.add = hc; a.add_ps = hstride; a.ai0 = L.ext;
+        } else {
+            mode = CG_DOWN;
+            a.A = L.S + static_cast<size_t>(m0) * L.ppS; a.rows = L.n3; a.K = L.next;
+            a.src = d_edge; a.src_ps = NE; a.bi0 = L.gext;
+            a.add = L.w3; a.add_ps = static_cast<long long>(L.nodes) * L.n3;
+            a.dst = d_edge; a.dst_ps = NE; a.so0 = L.g3;
+        }
+        const int bm = 8 * cfg.MT * cg_wm(cfg.WN);
+        a.nrowblk = (a.rows + bm - 1) / bm;
+        const int ncb = (L.nodes * R2 + 8 * cfg.WN - 1) / (8 * cfg.WN);
+        tbeg(s);
+        cg_run_mode(mode, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
+        tend(cls, s);
+        return REXP_OK;
+    }
+    const int NB = pick_nb(L.nodes, R2, shared);
+    GemvArgs g;
+    if (kind == 0) {
+        g = gemv_shape(L.n3, L.n3, L.nodes, shared);
+        g.M = L.X + static_cast<size_t>(m0) * L.ppX; g.xsrc = hc; g.xsrc_ps = hstride; g.xi0 = L.ia3; g.xi1 = L.ib3;
+        g.ydst = L.w3; g.ydst_ps = static_cast<long long>(L.nodes) * L.n3;
+    } else if (kind == 1) {
+        g = gemv_shape(L.next, L.n3, L.nodes, shared);
+        g.M = L.Y + static_cast<size_t>(m0) * L.ppY; g.xsrc = L.w3; g.xsrc_ps = static_cast<long long>(L.nodes) * L.n3;
+        g.ysrc = hc; g.ysrc_ps = hstride; g.yi = L.ext;
+        g.ydst = hp; g.ydst_ps = hstride;
+    } else {
+        g = gemv_shape(L.n3, L.next, L.nodes, shared);
+        g.M = L.S + static_cast<size_t>(m0) * L.ppS; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
+        g.ysrc = L.w3; g.ysrc_ps = static_cast<long long>(L.nodes) * L.n3;
+        g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
+    }
+    const dim3 grid((L.nodes / NB) * g.nrowblk, pc);
+    const size_t smem = gemv_smem(g, NB, R2);
+    tbeg(s);
+    if (kind == 0) launch_gemv<MODE_UPX>(R2, NB, grid, smem, s, g);
+    else if (kind == 1) launch_gemv<MODE_UPY>(R2, NB, grid, smem, s, g);
+    else launch_gemv<MODE_DOWN>(R2, NB, grid, smem, s, g);
+    tend(cls, s);
+    return REXP_OK;
+}
+
+// default stage choices, then (REXP_AUTOTUNE != 0) time every candidate on the
+// real buffers and keep the fastest: DMMA GEMM tiles MT in {2, 4} x WN in
+// {2, 4, 8} (shared store) and the GEMV kernel (nrhs <= 4)
+int DeviceStore::tune_stages() {
+    const size_t nl = levels.size();
+    t_upx.assign(nl, StageCfg());
+    t_upy.assign(nl, StageCfg());
+    t_down.assign(nl, StageCfg());
+    const bool gemv_ok = R2 == 2 || R2 == 4 || R2 == 8;   // GEMV kernels are compiled for these
+    for (size_t li = 0; li < nl; ++li) {
+        const Level& L = levels[li];
+        const bool use_gemm = shared && (L.nodes * R2 >= 4 || !gemv_ok);
+        StageCfg c;
+        c.kind = use_gemm ? 0 : 1;
+        cg_tile(L.n3, L.nodes * R2, c.MT, c.WN);
+        t_upx[li] = c;
+        t_down[li] = c;
+        cg_tile(L.next, L.nodes * R2, c.MT, c.WN);
+        t_upy[li] = c;
+    }
+    t_root = StageCfg();
+    t_root.kind = (shared && (R2 > 2 || !gemv_ok)) ? 0 : 1;
+    cg_tile(ns, R2, t_root.MT, t_root.WN);
+    const char* env = std::getenv("REXP_AUTOTUNE");
+    if ((env && std::string(env) == "0") || !shared) return REXP_OK;
+
+    const int pc = chunk;
+    cudaStream_t s = nullptr;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const bool saved_timing = timing;
+    timing = false;
+    auto time_cfg = [&](int kind, size_t li, const StageCfg& c) -> float {
+        if (launch_stage(kind, li, c, 0, pc, s) != REXP_OK) return 1e30f;
+        cudaEventRecord(e0, s);
+        for (int r = 0; r < 3; ++r) launch_stage(kind, li, c, 0, pc, s);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        if (cudaGetLastError() != cudaSuccess) return 1e30f;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        return ms;
+    };
+    auto tune = [&](int kind, size_t li, StageCfg& best) {
+        std::vector<StageCfg> cands;
+        for (int mt : {2, 4})
+            for (int wn : {2, 4, 8}) {
+                StageCfg c;
+                c.kind = 0; c.MT = mt; c.WN = wn;
+                cands.push_back(c);
+            }
+        if (gemv_ok) {
+            StageCfg c;
+            c.kind = 1;
+            cands.push_back(c);
+        }
+        float bt = time_cfg(kind, li, best);
+        for (const StageCfg& c : cands) {
+            const float t = time_cfg(kind, li, c);
+            if (t < bt) { bt = t; best = c; }
+        }
+    };
+    for (size_t li = 0; li < nl; ++li) {
+        tune(0, li, t_upx[li]);
+        tune(1, li, t_upy[li]);
+        tune(2, li, t_down[li]);
+    }
+    tune(3, 0, t_root);
+    timing = saved_timing;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return check("tune_stages");
+}
+
 // leaf solves and merge sweeps for local half poles [m0, m0 + pc) (work buffers are chunk-local)
 int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     const double2* cF = d_cF + static_cast<size_t>(m0) * nF;
@@ -1164,7 +1274,7 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
         a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
         const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
         tbeg(s);
-        cg_run<CG_LEAF_UP>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
+        cg_run_mode(CG_LEAF_UP, R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
         tend(T_LEAF_UP, s);
         FluxArgs fa{};
         fa.w = d_w; fa.h = d_h[0]; fa.D = d_D; fa.c1 = c1; fa.hps = hstride; fa.q = q; fa.nelem = nelem; fa.R2 = R2;
@@ -1189,115 +1299,19 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     }
     // ---- merges up ----
     for (size_t li = 0; li < levels.size(); ++li) {
-        Level& L = levels[li];
-        const double2* hc = d_h[li % 2];
-        double2* hp = d_h[(li + 1) % 2];
-        const double2* X = L.X + static_cast<size_t>(m0) * L.ppX;
-        const double2* Y = L.Y + static_cast<size_t>(m0) * L.ppY;
-        if (shared && L.nodes * R2 >= 4) {
-            int MT, WN;
-            {  // X stage: w3 = Xneg (h^a_3 + h^b_3)
-                CgemmArgs a{};
-                a.A = X; a.rows = L.n3; a.K = L.n3; a.nodes = L.nodes; a.R2 = R2;
-                a.src = hc; a.src_ps = hstride; a.bi0 = L.ia3; a.bi1 = L.ib3;
-                a.dst = L.w3; a.dst_ps = static_cast<long long>(L.nodes) * L.n3;
-                cg_tile(L.n3, L.nodes * R2, MT, WN);
-                a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
-                const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
-                tbeg(s);
-                cg_run<CG_UPX>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
-                tend(T_MERGE_UP, s);
-            }
-            {  // Y stage: h = h_child[ext] + Y w3
-                CgemmArgs a{};
-                a.A = Y; a.rows = L.next; a.K = L.n3; a.nodes = L.nodes; a.R2 = R2;
-                a.src = L.w3; a.src_ps = static_cast<long long>(L.nodes) * L.n3;
-                a.dst = hp; a.dst_ps = hstride; a.add = hc; a.add_ps = hstride; a.ai0 = L.ext;
-                cg_tile(L.next, L.nodes * R2, MT, WN);
-                a.nrowblk = (L.next + 8 * MT - 1) / (8 * MT);
-                const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
-                tbeg(s);
-                cg_run<CG_UPY>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
-                tend(T_MERGE_UP, s);
-            }
-            continue;
-        }
-        const int NB = pick_nb(L.nodes, R2, shared);
-        {  // X stage
-            GemvArgs g = gemv_shape(L.n3, L.n3, L.nodes, shared);
-            g.M = X; g.xsrc = hc; g.xsrc_ps = hstride; g.xi0 = L.ia3; g.xi1 = L.ib3;
-            g.ydst = L.w3; g.ydst_ps = static_cast<long long>(L.nodes) * L.n3;
-            dim3 grid((L.nodes / NB) * g.nrowblk, pc);
-            tbeg(s);
-            launch_gemv<MODE_UPX>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
-            tend(T_MERGE_UP, s);
-        }
-        {  // Y stage
-            GemvArgs g = gemv_shape(L.next, L.n3, L.nodes, shared);
-            g.M = Y; g.xsrc = L.w3; g.xsrc_ps = static_cast<long long>(L.nodes) * L.n3;
-            g.ysrc = hc; g.ysrc_ps = hstride; g.yi = L.ext;
-            g.ydst = hp; g.ydst_ps = hstride;
-            dim3 grid((L.nodes / NB) * g.nrowblk, pc);
-            tbeg(s);
-            launch_gemv<MODE_UPY>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
-            tend(T_MERGE_UP, s);
-        }
+        int rc;
+        if ((rc = launch_stage(0, li, t_upx[li], m0, pc, s))) return rc;
+        if ((rc = launch_stage(1, li, t_upy[li], m0, pc, s))) return rc;
     }
     // ---- periodic closure ----
     {
-        const double2* hr = d_h[levels.size() % 2];
-        const double2* Xr = d_Xroot + static_cast<size_t>(m0) * pp_Xroot;
-        if (shared && R2 > 2) {
-            CgemmArgs a{};
-            a.A = Xr; a.rows = ns; a.K = ns; a.nodes = 1; a.R2 = R2;
-            a.src = hr; a.src_ps = hstride; a.bi0 = d_rpos1; a.bi1 = d_rpos2;
-            a.dst = d_edge; a.dst_ps = NE; a.so0 = d_rgs;
-            int MT, WN;
-            cg_tile(ns, R2, MT, WN);
-            a.nrowblk = (ns + 8 * MT - 1) / (8 * MT);
-            const int ncb = (R2 + 8 * WN - 1) / (8 * WN);
-            tbeg(s);
-            cg_run<CG_ROOT>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
-            tend(T_ROOT, s);
-        } else {
-            GemvArgs g = gemv_shape(ns, ns, 1, true);
-            g.shared = 1;
-            g.M = Xr; g.xsrc = hr; g.xsrc_ps = hstride; g.xi0 = d_rpos1; g.xi1 = d_rpos2;
-            g.ydst = d_edge; g.ydst_ps = NE; g.yo = d_rgs;
-            dim3 grid(g.nrowblk, pc);
-            tbeg(s);
-            launch_gemv<MODE_ROOT>(R2, 1, grid, gemv_smem(g, 1, R2), s, g);
-            tend(T_ROOT, s);
-        }
+        int rc;
+        if ((rc = launch_stage(3, 0, t_root, m0, pc, s))) return rc;
     }
     // ---- merges down ----
     for (int li = static_cast<int>(levels.size()) - 1; li >= 0; --li) {
-        Level& L = levels[li];
-        const double2* S = L.S + static_cast<size_t>(m0) * L.ppS;
-        if (shared && L.nodes * R2 >= 4) {
-            CgemmArgs a{};
-            a.A = S; a.rows = L.n3; a.K = L.next; a.nodes = L.nodes; a.R2 = R2;
-            a.src = d_edge; a.src_ps = NE; a.bi0 = L.gext;
-            a.add = L.w3; a.add_ps = static_cast<long long>(L.nodes) * L.n3;
-            a.dst = d_edge; a.dst_ps = NE; a.so0 = L.g3;
-            int MT, WN;
-            cg_tile(L.n3, L.nodes * R2, MT, WN);
-            a.nrowblk = (L.n3 + 8 * MT - 1) / (8 * MT);
-            const int ncb = (L.nodes * R2 + 8 * WN - 1) / (8 * WN);
-            tbeg(s);
-            cg_run<CG_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
-            tend(T_MERGE_DOWN, s);
-            continue;
-        }
-        const int NB = pick_nb(L.nodes, R2, shared);
-        GemvArgs g = gemv_shape(L.n3, L.next, L.nodes, shared);
-        g.M = S; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
-        g.ysrc = L.w3; g.ysrc_ps = static_cast<long long>(L.nodes) * L.n3;
-        g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
-        dim3 grid((L.nodes / NB) * g.nrowblk, pc);
-        tbeg(s);
-        launch_gemv<MODE_DOWN>(R2, NB, grid, gemv_smem(g, NB, R2), s, g);
-        tend(T_MERGE_DOWN, s);
+        int rc;
+        if ((rc = launch_stage(2, static_cast<size_t>(li), t_down[li], m0, pc, s))) return rc;
     }
     // ---- leaves down ----
     if (fdm && fuse_sum) {
@@ -1319,7 +1333,7 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
         a.nrowblk = (q2 + 8 * MT - 1) / (8 * MT);
         const int ncb = (nelem * R2 + 8 * WN - 1) / (8 * WN);
         tbeg(s);
-        cg_run<CG_LEAF_DOWN>(R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
+        cg_run_mode(CG_LEAF_DOWN, R2, MT, WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
         tend(T_LEAF_DOWN, s);
     } else {
         LeafDownArgs a{};

@@ -10,6 +10,11 @@
 namespace rexp {
 namespace dev {
 
+struct StageCfg {
+    int kind = 0;   // 0: DMMA GEMM (k_cgemm), 1: GEMV (k_gemv)
+    int MT = 4, WN = 8;
+};
+
 struct Level {
     int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0;
     double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
@@ -74,8 +79,13 @@ class DeviceStore {
     double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_Epart = nullptr;
     int pgroup = 1, ngroups = 1;
     int chunk = 1;             // half poles per work-buffer chunk
+    int num_sms = 148;
     size_t pp_Ainv = 0, pp_Sleaf = 0, pp_Xroot = 0;
     int tree_chunk(int m0, int pc, cudaStream_t s);
+    int launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, int pc, cudaStream_t s);
+    int tune_stages();
+    std::vector<StageCfg> t_upx, t_upy, t_down;
+    StageCfg t_root;
     int pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s);
     double2 *d_Ainv = nullptr, *d_Sleaf = nullptr, *d_Xroot = nullptr;
     double2 *d_w = nullptr, *d_edge = nullptr;
