@@ -153,6 +153,9 @@ int rexp_get_poles(const rexp_handle* h, double* alpha, double* b);
 int rexp_get_accuracy(const rexp_handle* h, double* err, double* maxmod);
 /* node coordinates x[N], y[N] (host pointers) in the ordering above */
 int rexp_node_coords(const rexp_handle* h, double* x, double* y);
+/* the same without a handle (e.g. to sample kappa before rexp_setup) */
+int64_t rexp_mesh_num_nodes(int32_t n, int32_t p);
+int rexp_mesh_coords(int32_t n, int32_t p, double* x, double* y);
 /* bytes of the device operator store / of the per-step work buffers */
 int64_t rexp_store_bytes(const rexp_handle* h);
 int64_t rexp_work_bytes(const rexp_handle* h);

@@ -35,6 +35,8 @@ SIGNATURES = [
     ("rexp_get_poles", ctypes.c_int, [_P, _D, _D]),
     ("rexp_get_accuracy", ctypes.c_int, [_P, _D, _D]),
     ("rexp_node_coords", ctypes.c_int, [_P, _D, _D]),
+    ("rexp_mesh_num_nodes", ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
+    ("rexp_mesh_coords", ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _D, _D]),
     ("rexp_store_bytes", ctypes.c_int64, [_P]),
     ("rexp_work_bytes", ctypes.c_int64, [_P]),
     ("rexp_launches_per_step", ctypes.c_int32, [_P]),

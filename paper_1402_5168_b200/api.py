@@ -87,6 +87,18 @@ class Handle:
             pass
 
 
+def mesh_coords(n, p):
+    """Node coordinates (x, y) of the n x n element, p x p node mesh (no setup needed)."""
+    lib = _lib.load()
+    N = int(lib.rexp_mesh_num_nodes(n, p))
+    if N <= 0:
+        raise ValueError("invalid mesh")
+    x = np.zeros(N)
+    y = np.zeros(N)
+    _lib.check(lib.rexp_mesh_coords(n, p, _dptr(x), _dptr(y)), "rexp_mesh_coords")
+    return x, y
+
+
 def setup(model, n, p, tau, delta, Lambda, f=1.0, kappa=None, nrhs=1, store="auto", device=0,
           half_range=None, nthreads=0):
     """rexp_setup(L, tau, delta, Lambda): poles/weights + factorization + device store."""

@@ -230,6 +230,22 @@ int rexp_step_finish(rexp_handle* h, const double* e_dev, double* u_dev, void* s
 }
 
 int64_t rexp_num_nodes(const rexp_handle* h) { return h ? h->T.N : -1; }
+
+int64_t rexp_mesh_num_nodes(int32_t n, int32_t p) {
+    if (n < 2 || p < 4) return -1;
+    const int64_t q = p - 2;
+    return static_cast<int64_t>(n) * n * (q * q + 2 * q);
+}
+
+int rexp_mesh_coords(int32_t n, int32_t p, double* x, double* y) {
+    if (!x || !y) return REXP_EINVAL;
+    Tree T;
+    const int rc = build_tree(n, p, T);
+    if (rc) return rc;
+    std::memcpy(x, T.x.data(), T.x.size() * sizeof(double));
+    std::memcpy(y, T.y.data(), T.y.size() * sizeof(double));
+    return REXP_OK;
+}
 int32_t rexp_num_poles(const rexp_handle* h) { return h ? static_cast<int32_t>(h->ra.poles.size()) : -1; }
 int32_t rexp_num_half_poles(const rexp_handle* h) { return h ? static_cast<int32_t>(h->pt.alpha.size()) : -1; }
 

@@ -237,3 +237,29 @@ def test_config1_sampled_poles_against_oracle(c1_handle):
         print(f"config1 half pole {k} rel L2 {err:.3e}")
         assert err <= TOL
         hk.close()
+
+
+def test_config3_many_rhs_fourier_modes_closed_form():
+    """BASELINE config 3 (32x32 elements, p = 16, 64 RHS) in the bench's launch
+    configuration: every RHS is a different resolved Fourier mode, each checked
+    against expm(tau * symbol) after 2 steps."""
+    cfg = CONFIGS["c3_rsw_32x32_p16_x64"]
+    Lam = cfg["Lambda_tau"] / cfg["tau"]
+    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], nrhs=cfg["nrhs"])
+    x, y = h.node_coords()
+    rng = np.random.default_rng(9)
+    U, refs = [], []
+    f = cfg["f"]
+    for k in range(cfg["nrhs"]):
+        k1, k2 = (int(v) for v in rng.integers(-5, 6, size=2))
+        vec = rng.standard_normal(3) + 1j * rng.standard_normal(3)
+        ph = np.exp(2j * math.pi * (k1 * x + k2 * y))
+        a1, a2 = 2j * math.pi * k1, 2j * math.pi * k2
+        S = np.array([[0, -f, a1], [f, 0, a2], [a1, a2, 0]], dtype=complex)
+        U.append(vec[:, None] * ph[None, :])
+        refs.append((sla.expm(2 * cfg["tau"] * S) @ vec)[:, None] * ph[None, :])
+    got = _gpu_apply(h, np.stack(U), 2)
+    err = max(np.abs(got[k] - refs[k]).max() / np.abs(refs[k]).max() for k in range(cfg["nrhs"]))
+    print(f"config3 64-RHS Fourier-mode 2-step max error {err:.3e}")
+    assert err <= 1e-9
+    h.close()

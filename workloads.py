@@ -29,6 +29,10 @@ CONFIGS = {
                               nsteps=50, nrhs=1, seed=1234),
     "c3_rsw_32x32_p16_x64": dict(model="rsw", n=32, p=16, f=1.0, Lambda_tau=60.0, tau=0.25, delta=1e-10,
                                  nsteps=50, nrhs=64, seed=1234),
+    # reduced-size stand-in for c2 that fits one B200 (per-node store ~10 GB):
+    # the variable-coefficient (HBM-bound GEMV) path at a measurable scale
+    "c2r_wave_8x8_p16": dict(model="wave", n=8, p=16, Lambda_tau=20.0, tau=0.2, delta=1e-10,
+                             nsteps=10, nrhs=1, seed=1234),
     "c4_wave_64x64_p12": dict(model="wave", n=64, p=12, Lambda_tau=160.0, tau=0.5, delta=1e-10,
                               nsteps=200, nrhs=1, seed=1234),
 }
