@@ -19,8 +19,13 @@ namespace rexp {
 namespace dev {
 
 constexpr int FDM_T = 16;          // padded tile edge
-constexpr int FDM_LDT = 20;        // tile stride: conflict-free for transposed fragment reads
-constexpr int FDM_LDD = FDM_LDT;   // (the single direct read, stage 1, takes 2-way conflicts)
+constexpr int FDM_LDT = 16;        // tile stride (complex elements), XOR-swizzled columns:
+constexpr int FDM_LDD = FDM_LDT;
+// element (r, c) of a 16x16 complex tile lives at tix(r, c); the swizzle makes
+// both the DMMA C-fragment stores (row g, cols 2t4+{0,1}) and the transposed
+// B-fragment loads (row n = g, col k = t4) hit 8 distinct 16-byte slots per
+// quarter warp (searched exhaustively)
+__device__ __forceinline__ int tix(int r, int c) { return r * FDM_T + (c ^ ((5 * r) & 15)); }
 constexpr int FDM_WARPS = 8;
 constexpr int FDM_TILE_ELEMS = 2 * FDM_T * FDM_LDT + 4 * 16;     // tiles X, Y + boundary values
 
@@ -75,7 +80,7 @@ __device__ __forceinline__ void fdm_stage(const double* As, const double2* X, in
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
             const int n = nt * 8 + g;
-            b[nt] = TRANS ? X[n * LD + k] : X[k * LD + n];
+            b[nt] = TRANS ? X[tix(n, k)] : X[tix(k, n)];
         }
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
@@ -85,6 +90,29 @@ __device__ __forceinline__ void fdm_stage(const double* As, const double2* X, in
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) dmma884r(ci[mt][nt][0], ci[mt][nt][1], af[mt], b[nt].y);
+    }
+}
+
+// Stage 1 with B = T held in registers in fragment layout: bf[ks][nt] = T[ks*4+t4][nt*8+g].
+__device__ __forceinline__ void fdm_stage_reg(const double* As, const double2 (&bf)[4][2], int g, int t4,
+                                              double (&cr)[2][2][2], double (&ci)[2][2][2]) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) cr[mt][nt][0] = cr[mt][nt][1] = ci[mt][nt][0] = ci[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+        double af[2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) af[mt] = As[(mt * 8 + g) * FDM_LDV + ks * 4 + t4];   // A[m][k]
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) dmma884r(cr[mt][nt][0], cr[mt][nt][1], af[mt], bf[ks][nt].x);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) dmma884r(ci[mt][nt][0], ci[mt][nt][1], af[mt], bf[ks][nt].y);
     }
 }
 
@@ -100,56 +128,27 @@ __device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int
     const double2 c0 = cf[0];
     const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0, 0);
     const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0, 0);
-    // issue every global load of this problem up front (boundary values, the
-    // pole-independent fields of the 8 tile elements this lane forms)
-    double2 ubv[2];
+    // boundary values of this leaf (DOWN) into the warp's UB area
     if (DOWN) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int b = lane + 32 * u;
-            ubv[u] = b < nb ? a.edge[((size_t)m * a.NE + a.gB[(size_t)leaf * nb + b]) * a.R2 + r2]
-                            : make_double2(0.0, 0.0);
-        }
-    }
-    double fv[8][3];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const int e = lane + 32 * u;
-        const int i = e % FDM_T, j = e / FDM_T;
-        fv[u][0] = fv[u][1] = fv[u][2] = 0.0;
-        if (i < q && j < q) {
-            const double* f = a.F + ((size_t)((size_t)leaf * q2 + j * q + i) * a.nF) * a.R2 + r2;
-            fv[u][0] = f[0];
-            if (a.nF > 1) fv[u][1] = f[a.R2];
-            if (a.nF > 2) fv[u][2] = f[2 * a.R2];
-        }
-    }
-    if (DOWN) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-            if (lane + 32 * u < nb) UB[lane + 32 * u] = ubv[u];
+        for (int b = lane; b < nb; b += 32)
+            UB[b] = a.edge[((size_t)m * a.NE + a.gB[(size_t)leaf * nb + b]) * a.R2 + r2];
         __syncwarp();
     }
+    // T directly in B-fragment layout: this lane's 8 elements T[i = ks*4+t4][j = nt*8+g]
+    double fv[4][2][3];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const int e = lane + 32 * u;
-        const int i = e % FDM_T, j = e / FDM_T;
-        double2 v = make_double2(0.0, 0.0);
-        if (i < q && j < q) {
-            v.x = c0.x * fv[u][0] + c1v.x * fv[u][1] + c2v.x * fv[u][2];
-            v.y = c0.y * fv[u][0] + c1v.y * fv[u][1] + c2v.y * fv[u][2];
-            if (DOWN) {
-                // A_IB u_B at interior (i+1, j+1): row i+1 meets left/right, column j+1 meets bottom/top
-                const double dl = a.D2[(i + 1) * p + 0], dr = a.D2[(i + 1) * p + (p - 1)];
-                const double db = a.D2[(j + 1) * p + 0], dt = a.D2[(j + 1) * p + (p - 1)];
-                const double2 ul = UB[3 * q + j], ur = UB[q + j], ub = UB[i], ut = UB[2 * q + i];
-                v.x -= a.c2 * (dl * ul.x + dr * ur.x + db * ub.x + dt * ut.x);
-                v.y -= a.c2 * (dl * ul.y + dr * ur.y + db * ub.y + dt * ut.y);
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int i = ks * 4 + t4, j = nt * 8 + g;
+            fv[ks][nt][0] = fv[ks][nt][1] = fv[ks][nt][2] = 0.0;
+            if (i < q && j < q) {
+                const double* f = a.F + ((size_t)((size_t)leaf * q2 + j * q + i) * a.nF) * a.R2 + r2;
+                fv[ks][nt][0] = f[0];
+                if (a.nF > 1) fv[ks][nt][1] = f[a.R2];
+                if (a.nF > 2) fv[ks][nt][2] = f[2 * a.R2];
             }
         }
-        P[i * FDM_LDD + j] = v;
-    }
-    __syncwarp();
     // D^-1 entries of this lane's stage-2 fragments, fetched while stages 1-2 run
     const double2* dv = a.Dinv + (size_t)m * FDM_T * FDM_T;
     double2 dinv[2][2][2];
@@ -159,15 +158,36 @@ __device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int c = 0; c < 2; ++c) dinv[mt][nt][c] = __ldg(dv + (nt * 8 + 2 * t4 + c) * FDM_T + mt * 8 + g);
+    double2 bf[4][2];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int i = ks * 4 + t4, j = nt * 8 + g;
+            double2 v = make_double2(0.0, 0.0);
+            if (i < q && j < q) {
+                v.x = c0.x * fv[ks][nt][0] + c1v.x * fv[ks][nt][1] + c2v.x * fv[ks][nt][2];
+                v.y = c0.y * fv[ks][nt][0] + c1v.y * fv[ks][nt][1] + c2v.y * fv[ks][nt][2];
+                if (DOWN) {
+                    // A_IB u_B at interior (i+1, j+1): row i+1 meets left/right, column j+1 meets bottom/top
+                    const double dl = a.D2[(i + 1) * p + 0], dr = a.D2[(i + 1) * p + (p - 1)];
+                    const double db = a.D2[(j + 1) * p + 0], dt = a.D2[(j + 1) * p + (p - 1)];
+                    const double2 ul = UB[3 * q + j], ur = UB[q + j], ub = UB[i], ut = UB[2 * q + i];
+                    v.x -= a.c2 * (dl * ul.x + dr * ur.x + db * ub.x + dt * ut.x);
+                    v.y -= a.c2 * (dl * ul.y + dr * ur.y + db * ub.y + dt * ut.y);
+                }
+            }
+            bf[ks][nt] = v;
+        }
     // stage 1: S1 = Vinv T            (contract i)        -> Q[i'][j]
-    fdm_stage<false, FDM_LDD>(vif, P, g, t4, cr, ci);
+    fdm_stage_reg(vif, bf, g, t4, cr, ci);
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int c = 0; c < 2; ++c)
-                Q[(mt * 8 + g) * FDM_LDT + nt * 8 + 2 * t4 + c] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
+                Q[tix(mt * 8 + g, nt * 8 + 2 * t4 + c)] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
     __syncwarp();
     // stage 2: S2^T = Vinv S1^T       (contract j) -> C[j'][i'], scaled by Dinv (symmetric) -> P[j'][i']
     fdm_stage<true, FDM_LDT>(vif, Q, g, t4, cr, ci);
@@ -180,7 +200,7 @@ __device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int
                 const int jp = mt * 8 + g, ip = nt * 8 + 2 * t4 + c;
                 const double2 d = dinv[mt][nt][c];
                 const double xr = cr[mt][nt][c], xi = ci[mt][nt][c];
-                P[jp * FDM_LDT + ip] = make_double2(xr * d.x - xi * d.y, xr * d.y + xi * d.x);
+                P[tix(jp, ip)] = make_double2(xr * d.x - xi * d.y, xr * d.y + xi * d.x);
             }
     __syncwarp();
     // stage 3: S3 = V W               (contract i'), W[i'][j'] = P[j'][i']  -> Q[i][j']
@@ -191,7 +211,7 @@ __device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int c = 0; c < 2; ++c)
-                Q[(mt * 8 + g) * FDM_LDT + nt * 8 + 2 * t4 + c] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
+                Q[tix(mt * 8 + g, nt * 8 + 2 * t4 + c)] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
     __syncwarp();
     // stage 4: U^T = V S3^T           (contract j') -> C[j][i] = U[i][j]
     fdm_stage<true, FDM_LDT>(vf, Q, g, t4, cr, ci);
@@ -301,7 +321,7 @@ __global__ void __launch_bounds__(32 * FDM_WARPS, 2) k_leaf_fdm(FdmArgs a) {
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int j = mt * 8 + g, i = nt * 8 + 2 * t4 + c;
-                P[i * FDM_LDD + j] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
+                P[tix(i, j)] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
             }
     __syncwarp();
     for (int b = lane; b < nb; b += 32) {
@@ -311,7 +331,7 @@ __global__ void __launch_bounds__(32 * FDM_WARPS, 2) k_leaf_fdm(FdmArgs a) {
         double sx = 0.0, sy = 0.0;
         for (int k = 0; k < q; ++k) {
             // bottom/top: U[i = s1][j = k];  right/left: U[i = k][j = s1]
-            const double2 u = (side == 0 || side == 2) ? P[s1 * FDM_LDD + k] : P[k * FDM_LDD + s1];
+            const double2 u = (side == 0 || side == 2) ? P[tix(s1, k)] : P[tix(k, s1)];
             const double dk = drow[k + 1];
             sx = fma(dk, u.x, sx);
             sy = fma(dk, u.y, sy);
