@@ -351,6 +351,7 @@ def run_ours(args, cfg):
                        "baseline_nodes_per_field_convention": cfg["n"] ** 2 * cfg["p"] ** 2,
                        "store": "shared" if cfg["model"] == "rsw" else "pernode",
                        "leaf_solver": h.leaf_solver,
+                       "merge_kernels": h.stage_report,
                        "store_bytes": h.store_bytes, "work_bytes": h.work_bytes,
                        "l2": "operator store + work buffers exceed the 126 MB L2 (no flush needed)",
                        "parallelism": f"pole-sharded x{world}" if world > 1 else "single GPU"},

@@ -164,6 +164,9 @@ int32_t rexp_launches_per_step(const rexp_handle* h);
 /* leaf solver of the device store: 0 = dense q^2 x q^2 leaf operators,
  * 1 = tensor-product leaf inverse (constant coefficients), -1 = no device store */
 int32_t rexp_leaf_solver(const rexp_handle* h);
+/* kernel chosen for every merge stage (X, Y, down per level) and the closure
+ * by the setup-time autotuner, as text (for reports) */
+int rexp_stage_report(const rexp_handle* h, char* buf, int32_t len);
 
 /* ---- per-kernel timing (bench) ----
  * Between rexp_timing_begin and rexp_timing_end every kernel launch of the

@@ -41,6 +41,7 @@ SIGNATURES = [
     ("rexp_work_bytes", ctypes.c_int64, [_P]),
     ("rexp_launches_per_step", ctypes.c_int32, [_P]),
     ("rexp_leaf_solver", ctypes.c_int32, [_P]),
+    ("rexp_stage_report", ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_int32]),
     ("rexp_timing_begin", ctypes.c_int, [_P]),
     ("rexp_timing_end", ctypes.c_int, [_P, _D, ctypes.POINTER(ctypes.c_int32)]),
     ("rexp_export_num_levels", ctypes.c_int32, [_P]),

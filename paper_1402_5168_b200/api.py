@@ -72,6 +72,12 @@ class Handle:
         return {0: "dense", 1: "tensor"}.get(v, None)
 
     @property
+    def stage_report(self):
+        buf = ctypes.create_string_buffer(4096)
+        _lib.check(_lib.load().rexp_stage_report(self.ptr, buf, 4096), "rexp_stage_report")
+        return buf.value.decode()
+
+    @property
     def partial_len(self):
         return int(_lib.load().rexp_partial_len(self.ptr))
 

@@ -153,6 +153,7 @@ int rexp_setup(const rexp_problem* prob, double tau, double delta, double Lambda
             if ((rc = factor_host(h->P, h->T, h->pt, c0, c1, h->shared, opt.nthreads, ops))) return rc;
             if ((rc = h->dev->upload_ops(ops, c0 - h->h0))) return rc;
         }
+        if ((rc = h->dev->tune_stages(true))) return rc;
     }
     *out = h.release();
     return REXP_OK;
@@ -289,6 +290,14 @@ int32_t rexp_launches_per_step(const rexp_handle* h) {
     return 6 + 3 * static_cast<int32_t>(h->T.levels.size());
 }
 
+
+int rexp_stage_report(const rexp_handle* h, char* buf, int32_t len) {
+    if (!h || !h->dev || !buf || len <= 0) return REXP_EINVAL;
+    const std::string s = h->dev->stage_report();
+    std::strncpy(buf, s.c_str(), static_cast<size_t>(len) - 1);
+    buf[len - 1] = 0;
+    return REXP_OK;
+}
 
 int32_t rexp_leaf_solver(const rexp_handle* h) {
     if (!h || !h->dev) return -1;

@@ -920,7 +920,7 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     configure_kernels();
-    return tune_stages();
+    return tune_stages(false);
 }
 
 // copy the host factorization of local half poles [m0, m0 + count) into the store
@@ -1171,7 +1171,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
 // default stage choices, then (REXP_AUTOTUNE != 0) time every candidate on the
 // real buffers and keep the fastest: DMMA GEMM tiles MT in {2, 4} x WN in
 // {2, 4, 8} (shared store) and the GEMV kernel (nrhs <= 4)
-int DeviceStore::tune_stages() {
+int DeviceStore::tune_stages(bool measure) {
     const size_t nl = levels.size();
     t_upx.assign(nl, StageCfg());
     t_upy.assign(nl, StageCfg());
@@ -1192,7 +1192,7 @@ int DeviceStore::tune_stages() {
     t_root.kind = (shared && (R2 > 2 || !gemv_ok)) ? 0 : 1;
     cg_tile(ns, R2, t_root.MT, t_root.WN);
     const char* env = std::getenv("REXP_AUTOTUNE");
-    if ((env && std::string(env) == "0") || !shared) return REXP_OK;
+    if (!measure || (env && std::string(env) == "0") || !shared) return REXP_OK;
 
     const int pc = chunk;
     cudaStream_t s = nullptr;
@@ -1201,16 +1201,29 @@ int DeviceStore::tune_stages() {
     cudaEventCreate(&e1);
     const bool saved_timing = timing;
     timing = false;
+    // each candidate is timed as it runs in a step: once, with a cold L2
+    // (a 256 MB write evicts the 126 MB L2 before every timed launch)
+    void* flush = nullptr;
+    const size_t flush_bytes = size_t(256) << 20;
+    if (cudaMalloc(&flush, flush_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        flush = nullptr;
+    }
     auto time_cfg = [&](int kind, size_t li, const StageCfg& c) -> float {
         if (launch_stage(kind, li, c, 0, pc, s) != REXP_OK) return 1e30f;
-        cudaEventRecord(e0, s);
-        for (int r = 0; r < 3; ++r) launch_stage(kind, li, c, 0, pc, s);
-        cudaEventRecord(e1, s);
-        cudaEventSynchronize(e1);
-        if (cudaGetLastError() != cudaSuccess) return 1e30f;
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
-        return ms;
+        float total = 0.f;
+        for (int r = 0; r < 3; ++r) {
+            if (flush) cudaMemsetAsync(flush, r, flush_bytes, s);
+            cudaEventRecord(e0, s);
+            launch_stage(kind, li, c, 0, pc, s);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            if (cudaGetLastError() != cudaSuccess) return 1e30f;
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            total += ms;
+        }
+        return total;
     };
     auto tune = [&](int kind, size_t li, StageCfg& best) {
         std::vector<StageCfg> cands;
@@ -1238,9 +1251,23 @@ int DeviceStore::tune_stages() {
     }
     tune(3, 0, t_root);
     timing = saved_timing;
+    tuned = true;
+    if (flush) cudaFree(flush);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return check("tune_stages");
+}
+
+std::string DeviceStore::stage_report() const {
+    auto one = [](const StageCfg& c) {
+        return c.kind == 1 ? std::string("gemv")
+                           : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN);
+    };
+    std::string s = tuned ? "tuned:" : "default:";
+    for (size_t li = 0; li < levels.size(); ++li)
+        s += " L" + std::to_string(li + 1) + "[" + one(t_upx[li]) + "," + one(t_upy[li]) + "," + one(t_down[li]) + "]";
+    s += " root[" + one(t_root) + "]";
+    return s;
 }
 
 // leaf solves and merge sweeps for local half poles [m0, m0 + pc) (work buffers are chunk-local)

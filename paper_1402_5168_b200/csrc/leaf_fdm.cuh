@@ -61,7 +61,7 @@ __device__ __forceinline__ void dmma884r(double& c0, double& c1, double a, doubl
 
 // C (16x16 complex, in fragments) = A (16x16 real, fragments af) * B, where
 // B[k][n] = TRANS ? X[n*LD + k] : X[k*LD + n]  (complex tile in shared memory).
-constexpr int FDM_LDV = 18;        // stride of V, V^-1 in shared memory
+constexpr int FDM_LDV = 20;        // stride of V, V^-1 in shared memory (conflict-free per half warp)
 
 template <bool TRANS, int LD>
 __device__ __forceinline__ void fdm_stage(const double* As, const double2* X, int g, int t4,
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(32 * FDM_WARPS, 2) k_leaf_fdm(FdmArgs a) {
         vif[r * FDM_LDV + c] = a.Vinv[e];
     }
     __syncthreads();
-    double2* P = fsm + FDM_T * FDM_LDV + (size_t)warp * FDM_TILE_ELEMS;   // 2*16*18 doubles = 16*18 double2
+    double2* P = fsm + FDM_T * FDM_LDV + (size_t)warp * FDM_TILE_ELEMS;   // V, V^-1: 2 x 16 x FDM_LDV doubles
     double2* Q = P + FDM_T * FDM_LDT;
     double2* UB = Q + FDM_T * FDM_LDT;
     double cr[2][2][2], ci[2][2][2];

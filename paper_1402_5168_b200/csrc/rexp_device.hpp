@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
 #include <vector>
 
 #include "rexp_internal.hpp"
@@ -83,7 +84,11 @@ class DeviceStore {
     size_t pp_Ainv = 0, pp_Sleaf = 0, pp_Xroot = 0;
     int tree_chunk(int m0, int pc, cudaStream_t s);
     int launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, int pc, cudaStream_t s);
-    int tune_stages();
+    public:
+    int tune_stages(bool measure);   // heuristic defaults; measure = time the candidates (after upload)
+    std::string stage_report() const;
+    bool tuned = false;
+    private:
     std::vector<StageCfg> t_upx, t_upy, t_down;
     StageCfg t_root;
     int pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s);
