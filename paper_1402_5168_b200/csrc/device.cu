@@ -506,55 +506,6 @@ __global__ void k_pole_sum(PoleSumArgs a) {
 }
 
 // --------------------------------------------------------------------------
-// k_pole_sum_fused (tensor-product leaf path): interior nodes combine the
-// pole-group partials written by k_leaf_fdm<2> (group order), edge nodes sum
-// their per-pole values (ascending pole order).
-// --------------------------------------------------------------------------
-struct PoleSum2Args {
-    const double* Epart;    // [ngroups][nE][R2][NI]
-    const double2* edge;    // [nh][NE][R2]
-    const double2* dE;      // [nh][nE]
-    double* E;              // [nE][R2][N]
-    long long N, NI, NE;
-    int nh, nE, R2, ngroups;
-};
-
-__global__ void k_pole_sum_fused(PoleSum2Args a) {
-    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (tid >= a.N * a.R2) return;
-    const long long g = tid % a.N;
-    const int r2 = (int)(tid / a.N);
-    double s[3] = {0.0, 0.0, 0.0};
-    if (g < a.NI) {
-        for (int grp = 0; grp < a.ngroups; ++grp)
-            for (int k = 0; k < a.nE; ++k) s[k] += a.Epart[(((size_t)grp * a.nE + k) * a.R2 + r2) * a.NI + g];
-    } else {
-        const double2* base = a.edge + (g - a.NI) * a.R2 + r2;
-        const long long ps = a.NE * a.R2;
-        int m = 0;
-        for (; m + 4 <= a.nh; m += 4) {
-            double2 u[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = base[(size_t)(m + k) * ps];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                for (int e = 0; e < a.nE; ++e) {
-                    const double2 d = a.dE[(size_t)(m + k) * a.nE + e];
-                    s[e] += d.x * u[k].x - d.y * u[k].y;
-                }
-        }
-        for (; m < a.nh; ++m) {
-            const double2 u = base[(size_t)m * ps];
-            for (int e = 0; e < a.nE; ++e) {
-                const double2 d = a.dE[(size_t)m * a.nE + e];
-                s[e] += d.x * u.x - d.y * u.y;
-            }
-        }
-    }
-    for (int k = 0; k < a.nE; ++k) a.E[((size_t)k * a.R2 + r2) * a.N + g] = s[k];
-}
-
-// --------------------------------------------------------------------------
 // k_recover: new state from pole sums (velocity recovery, fused with the sum's output)
 // --------------------------------------------------------------------------
 struct RecoverArgs {
@@ -830,6 +781,15 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
                     Dinv[(static_cast<size_t>(m) * FDM_T + i) * FDM_T + j] = make_double2(v.real(), v.imag());
                 }
         }
+        // e0 = V^T d_0, e1 = V^T d_{p-1}, d_r[k] = D[r][k+1]: the flux of the
+        // particular solution in the spectral basis (UP pass)
+        std::vector<double> E01(2 * FDM_T, 0.0);
+        for (int c = 0; c < q; ++c)
+            for (int k = 0; k < q; ++k) {
+                E01[c] += V[static_cast<size_t>(k) * q + c] * ch.D[0 * p + k + 1];
+                E01[FDM_T + c] += V[static_cast<size_t>(k) * q + c] * ch.D[(p - 1) * p + k + 1];
+            }
+        if ((rc = put(&d_E01, E01))) return rc;
         if ((rc = put(&d_V, Vp))) return rc;
         if ((rc = put(&d_Vinv, Vip))) return rc;
         if ((rc = put(&d_Dinv, Dinv))) return rc;
@@ -884,10 +844,6 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         chunk = env ? std::max(1, std::atoi(env)) : static_cast<int>(std::max<size_t>(1, budget / per_pole));
         chunk = std::min(chunk, nh);
     }
-    {
-        const char* env = std::getenv("REXP_FUSE_SUM");
-        fuse_sum = fdm && chunk == nh && env && std::string(env) == "1";
-    }
     work_bytes = 0;
     auto walloc = [&](auto** pp, size_t count, size_t elt) -> int {
         work_bytes += static_cast<int64_t>(count * elt);
@@ -895,16 +851,7 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     };
     const size_t pc = static_cast<size_t>(chunk);
     if ((rc = walloc(&d_F, static_cast<size_t>(NI) * nF * R2, 8))) return rc;
-    if (!fuse_sum) {
-        if ((rc = walloc(&d_w, pc * NI * R2, 16))) return rc;
-    } else {
-        // pole groups for the fused downward leaf solve + interior pole sum
-        const long long per_group = static_cast<long long>(nelem) * R2;
-        ngroups = static_cast<int>(std::min<long long>(nh, std::max<long long>(1, (4736 + per_group - 1) / per_group)));
-        pgroup = (nh + ngroups - 1) / ngroups;
-        ngroups = (nh + pgroup - 1) / pgroup;
-        if ((rc = walloc(&d_Epart, static_cast<size_t>(ngroups) * nE * R2 * NI, 8))) return rc;
-    }
+    if ((rc = walloc(&d_w, pc * NI * R2, 16))) return rc;
     if ((rc = walloc(&d_edge, pc * NE * R2, 16))) return rc;
     if ((rc = walloc(&d_h[0], pc * hmax * R2, 16))) return rc;
     if ((rc = walloc(&d_h[1], pc * hmax * R2, 16))) return rc;
@@ -1056,7 +1003,6 @@ void DeviceStore::configure_kernels() {
     cg_allow_all();
     cudaFuncSetAttribute(k_leaf_fdm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_fdm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_fdm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
     allow_all<4>();
@@ -1278,12 +1224,10 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     // ---- leaves up ----
     FdmArgs fd{};
     if (fdm) {
-        fd.V = d_V; fd.Vinv = d_Vinv; fd.Dinv = d_Dinv + static_cast<size_t>(m0) * FDM_T * FDM_T;
+        fd.E01 = d_E01; fd.V = d_V; fd.Vinv = d_Vinv; fd.Dinv = d_Dinv + static_cast<size_t>(m0) * FDM_T * FDM_T;
         fd.D = d_D; fd.D2 = d_D2; fd.F = d_F; fd.cF = cF;
         fd.q = q; fd.p = p; fd.nF = nF; fd.nelem = nelem; fd.R2 = R2; fd.nh = pc; fd.c1 = c1; fd.c2 = c1 * c1;
         fd.h = d_h[0]; fd.hps = hstride; fd.edge = d_edge; fd.NE = NE; fd.gB = d_leaf_gB; fd.w = d_w;
-        fd.dE = d_dE + static_cast<size_t>(m0) * nE; fd.nE = nE; fd.pgroup = pgroup; fd.ngroups = ngroups;
-        fd.Epart = d_Epart;
     }
     const long long nprob = static_cast<long long>(pc) * nelem * R2;
     const unsigned fdm_blocks = static_cast<unsigned>((nprob + FDM_WARPS - 1) / FDM_WARPS);
@@ -1341,13 +1285,7 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
         if ((rc = launch_stage(2, static_cast<size_t>(li), t_down[li], m0, pc, s))) return rc;
     }
     // ---- leaves down ----
-    if (fdm && fuse_sum) {
-        // downward leaf solves fused with the interior pole sums (u_m stays on chip)
-        const long long nsum = static_cast<long long>(ngroups) * nelem * R2;
-        tbeg(s);
-        k_leaf_fdm<2><<<static_cast<unsigned>((nsum + FDM_WARPS - 1) / FDM_WARPS), 32 * FDM_WARPS, fdm_smem, s>>>(fd);
-        tend(T_LEAF_DOWN, s);
-    } else if (fdm) {
+    if (fdm) {
         tbeg(s);
         k_leaf_fdm<1><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
         tend(T_LEAF_DOWN, s);
@@ -1380,16 +1318,6 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
 }
 
 int DeviceStore::pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s) {
-    if (fuse_sum) {
-        PoleSum2Args a{};
-        a.Epart = d_Epart; a.edge = d_edge; a.dE = d_dE; a.E = d_E_out;
-        a.N = N; a.NI = NI; a.NE = NE; a.nh = pc; a.nE = nE; a.R2 = R2; a.ngroups = ngroups;
-        const long long tot = N * R2;
-        tbeg(s);
-        k_pole_sum_fused<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
-        tend(T_POLE_SUM, s);
-        return check("pole_sum");
-    }
     PoleSumArgs a{};
     a.accumulate = accumulate ? 1 : 0;
     a.w = d_w; a.edge = d_edge; a.dE = d_dE + static_cast<size_t>(m0) * nE; a.E = d_E_out;

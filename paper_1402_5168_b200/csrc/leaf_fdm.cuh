@@ -30,6 +30,7 @@ constexpr int FDM_WARPS = 8;
 constexpr int FDM_TILE_ELEMS = 2 * FDM_T * FDM_LDT + 4 * 16;     // tiles X, Y + boundary values
 
 struct FdmArgs {
+    const double* E01;      // 2 x 16: e0 = V^T d_0, e1 = V^T d_{p-1} (d_r[k] = D[r][k+1]), zero padded
     const double* V;        // 16 x 16 row-major, zero padded
     const double* Vinv;     // 16 x 16 row-major, zero padded
     const double2* Dinv;    // [nh][16*16] 1/(c2 (l_i + l_j) - sigma_m), zero padded
@@ -47,10 +48,6 @@ struct FdmArgs {
     long long NE;
     const int* gB;          // [nelem][4q]
     double2* w;             // [nh][nelem][q2][R2]
-    // DOWN_SUM
-    const double2* dE;      // [nh][nE]
-    int nE, pgroup, ngroups;
-    double* Epart;          // [ngroups][nE][R2][NI]
 };
 
 __device__ __forceinline__ void dmma884r(double& c0, double& c1, double a, double b) {
@@ -118,7 +115,7 @@ __device__ __forceinline__ void fdm_stage_reg(const double* As, const double2 (&
 
 // Right-hand side tile T (UP: f; DOWN: f - A_IB u_B) for pole m, then the
 // four stages; returns U[i][j] in fragments (cr, ci) at (j = mt*8+g, i = nt*8+2t4+c).
-template <bool DOWN>
+template <bool DOWN, bool HALF = false>
 __device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int r2, int lane, double2* P, double2* Q,
                                           double2* UB, const double* vf, const double* vif,
                                           double (&cr)[2][2][2], double (&ci)[2][2][2]) {
@@ -203,6 +200,7 @@ __device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int
                 P[tix(jp, ip)] = make_double2(xr * d.x - xi * d.y, xr * d.y + xi * d.x);
             }
     __syncwarp();
+    if (HALF) return;   // spectral coefficients W^T left in P (P[tix(j', i')] = W[i'][j'])
     // stage 3: S3 = V W               (contract i'), W[i'][j'] = P[j'][i']  -> Q[i][j']
     fdm_stage<true, FDM_LDT>(vf, P, g, t4, cr, ci);
 #pragma unroll
@@ -218,10 +216,8 @@ __device__ __forceinline__ void fdm_solve(const FdmArgs& a, int m, int leaf, int
     __syncwarp();   // P, Q reusable by the caller after this point
 }
 
-// MODE 0 = UP (h = N_I A^-1 f), 1 = DOWN (interior solution u_m written),
-// 2 = DOWN_SUM: a warp walks the half poles [grp*pg, grp*pg + pg) for one
-// (leaf, part) and accumulates the interior pole sums E_k = sum_m Re(d_mk u_m)
-// in ascending pole order (u_m never leaves the SM); partials per group.
+// MODE 0 = UP (h = N_I A^-1 f, from the spectral coefficients), 1 = DOWN
+// (interior solution u_m written for the pole sum).
 template <int MODE>
 __global__ void __launch_bounds__(32 * FDM_WARPS, 2) k_leaf_fdm(FdmArgs a) {
     extern __shared__ double2 fsm[];
@@ -243,64 +239,54 @@ __global__ void __launch_bounds__(32 * FDM_WARPS, 2) k_leaf_fdm(FdmArgs a) {
     double cr[2][2][2], ci[2][2][2];
     const long long prob = (long long)blockIdx.x * FDM_WARPS + warp;
 
-    if (MODE == 2) {
-        const long long nprob = (long long)a.ngroups * a.nelem * a.R2;
-        if (prob >= nprob) return;
-        const int r2 = (int)(prob % a.R2);
-        const int leaf = (int)((prob / a.R2) % a.nelem);
-        const int grp = (int)(prob / ((long long)a.R2 * a.nelem));
-        const int m0 = grp * a.pgroup, m1 = min(a.nh, m0 + a.pgroup);
-        double E[3][2][2][2];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt) E[k][mt][nt][0] = E[k][mt][nt][1] = 0.0;
-        for (int m = m0; m < m1; ++m) {
-            fdm_solve<true>(a, m, leaf, r2, lane, P, Q, UB, vf, vif, cr, ci);
-            const double2* dm = a.dE + (size_t)m * a.nE;
-            const double2 d0 = dm[0], d1 = dm[1];
-            const double2 d2 = a.nE > 2 ? dm[2] : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const double ur = cr[mt][nt][c], ui = ci[mt][nt][c];
-                        E[0][mt][nt][c] += d0.x * ur - d0.y * ui;
-                        E[1][mt][nt][c] += d1.x * ur - d1.y * ui;
-                        E[2][mt][nt][c] += d2.x * ur - d2.y * ui;
-                    }
-        }
-        // partial sums of this pole group at the leaf's interior nodes
-        const size_t NI = (size_t)a.nelem * q2;
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int j = mt * 8 + g, i = nt * 8 + 2 * t4 + c;
-                    if (i < q && j < q) {
-                        const size_t node = (size_t)leaf * q2 + j * q + i;
-#pragma unroll
-                        for (int k = 0; k < 3; ++k)
-                            if (k < a.nE) a.Epart[(((size_t)grp * a.nE + k) * a.R2 + r2) * NI + node] = E[k][mt][nt][c];
-                    }
-                }
-        return;
-    }
-
     const long long nprob = (long long)a.nh * a.nelem * a.R2;
     if (prob >= nprob) return;
     const int r2 = (int)(prob % a.R2);
     const int leaf = (int)((prob / a.R2) % a.nelem);
     const int m = (int)(prob / ((long long)a.R2 * a.nelem));
-    fdm_solve<MODE == 1>(a, m, leaf, r2, lane, P, Q, UB, vf, vif, cr, ci);
-
-    if (MODE == 1) {
+    if (MODE == 0) {
+        // UP needs only the boundary flux h = N_I A^-1 f.  With A^-1 f = V W V^T:
+        //   bottom/top  (d = D[0|p-1][1..q], row sums over j):  h = -/+ c1 V (W e),
+        //   left/right  (column sums over i):                    h = -/+ c1 V (W^T e),
+        // e = V^T d precomputed - four 16-vectors instead of stages 3-4.
+        fdm_solve<false, true>(a, m, leaf, r2, lane, P, Q, UB, vf, vif, cr, ci);
+        // y_s[r] = sum_c W[r][c] e_s[c]  (lanes 0-15),  z_s[r] = sum_c W[c][r] e_s[c]  (lanes 16-31);
+        // P holds W^T: P[tix(j', i')] = W[i'][j']
+        {
+            const int r = lane & 15;
+            const bool colsum = lane >= 16;
+            double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+#pragma unroll 4
+            for (int c = 0; c < FDM_T; ++c) {
+                const double2 wv = colsum ? P[tix(r, c)] : P[tix(c, r)];   // W[c][r] : W[r][c]
+                const double e0 = __ldg(a.E01 + c), e1 = __ldg(a.E01 + FDM_T + c);
+                acc0.x = fma(wv.x, e0, acc0.x); acc0.y = fma(wv.y, e0, acc0.y);
+                acc1.x = fma(wv.x, e1, acc1.x); acc1.y = fma(wv.y, e1, acc1.y);
+            }
+            // UB[0..15] = y0, [16..31] = y1, [32..47] = z0, [48..63] = z1
+            UB[(colsum ? 32 : 0) + r] = acc0;
+            UB[(colsum ? 48 : 16) + r] = acc1;
+        }
+        __syncwarp();
+        for (int b = lane; b < nb; b += 32) {
+            const int side = b / q, s1 = b % q;
+            // bottom: -V y0, right: +V z1, top: +V y1, left: -V z0  (index s1 = i or j)
+            const int src = side == 0 ? 0 : side == 1 ? 48 : side == 2 ? 16 : 32;
+            const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
+            double sx = 0.0, sy = 0.0;
+#pragma unroll 4
+            for (int k = 0; k < FDM_T; ++k) {
+                const double v = vf[s1 * FDM_LDV + k];
+                const double2 y = UB[src + k];
+                sx = fma(v, y.x, sx);
+                sy = fma(v, y.y, sy);
+            }
+            a.h[((size_t)m * a.hps + (size_t)leaf * nb + b) * a.R2 + r2] = make_double2(sgn * sx, sgn * sy);
+        }
+        return;
+    }
+    fdm_solve<true>(a, m, leaf, r2, lane, P, Q, UB, vf, vif, cr, ci);
+    {
         double2* wl = a.w + (((size_t)m * a.nelem + leaf) * q2) * a.R2 + r2;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
@@ -311,32 +297,6 @@ __global__ void __launch_bounds__(32 * FDM_WARPS, 2) k_leaf_fdm(FdmArgs a) {
                     const int j = mt * 8 + g, i = nt * 8 + 2 * t4 + c;
                     if (i < q && j < q) wl[(size_t)(j * q + i) * a.R2] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
                 }
-        return;
-    }
-    // UP: U into P, then the flux h = N_I u
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int j = mt * 8 + g, i = nt * 8 + 2 * t4 + c;
-                P[tix(i, j)] = make_double2(cr[mt][nt][c], ci[mt][nt][c]);
-            }
-    __syncwarp();
-    for (int b = lane; b < nb; b += 32) {
-        const int side = b / q, s1 = b % q;
-        const double* drow = a.D + ((side == 0 || side == 3) ? 0 : (p - 1) * p);
-        const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
-        double sx = 0.0, sy = 0.0;
-        for (int k = 0; k < q; ++k) {
-            // bottom/top: U[i = s1][j = k];  right/left: U[i = k][j = s1]
-            const double2 u = (side == 0 || side == 2) ? P[tix(s1, k)] : P[tix(k, s1)];
-            const double dk = drow[k + 1];
-            sx = fma(dk, u.x, sx);
-            sy = fma(dk, u.y, sy);
-        }
-        a.h[((size_t)m * a.hps + (size_t)leaf * nb + b) * a.R2 + r2] = make_double2(sgn * sx, sgn * sy);
     }
 }
 

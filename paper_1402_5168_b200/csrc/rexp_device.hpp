@@ -48,7 +48,6 @@ class DeviceStore {
     int h0 = 0, h1 = 0, nh = 0, nrhs = 1, R2 = 2, nF = 0, nE = 0, ns = 0, nroot_b = 0;
     bool shared = true;
     bool fdm = false;          // tensor-product leaf inverse (constant coefficients)
-    bool fuse_sum = false;     // REXP_FUSE_SUM=1: downward leaf solve fused with the interior pole sum
     double c1 = 0.0;
     std::vector<double> scal;
     int64_t store_bytes = 0, work_bytes = 0;
@@ -77,8 +76,7 @@ class DeviceStore {
     double *d_D = nullptr, *d_Dw = nullptr, *d_kappa = nullptr, *d_NI = nullptr, *d_F = nullptr;
     int *d_elem_g = nullptr, *d_leaf_gB = nullptr, *d_rpos1 = nullptr, *d_rpos2 = nullptr, *d_rgs = nullptr;
     double2 *d_cF = nullptr, *d_dE = nullptr, *d_Dinv = nullptr;
-    double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_Epart = nullptr;
-    int pgroup = 1, ngroups = 1;
+    double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_E01 = nullptr;
     int chunk = 1;             // half poles per work-buffer chunk
     int num_sms = 148;
     size_t pp_Ainv = 0, pp_Sleaf = 0, pp_Xroot = 0;
