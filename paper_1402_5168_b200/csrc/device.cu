@@ -27,7 +27,7 @@
 #include "rexp_device.hpp"
 #include "cgemm.cuh"
 #include "cgemm_launch.hpp"
-#include "leaf_fdm.cuh"
+#include "leaf_spec.cuh"
 
 namespace rexp {
 namespace dev {
@@ -453,14 +453,14 @@ struct PoleSumArgs {
     const double2* edge;    // edge solutions     [nh][NE][R2]
     const double2* dE;      // [nh][nE]
     double* E;              // [nE][R2][N]
-    long long N, NI, NE;
+    long long N, NI, NE, g0;
     int nh, nE, R2;
 };
 
 __global__ void k_pole_sum(PoleSumArgs a) {
     const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (tid >= a.N * a.R2) return;
-    const long long g = tid / a.R2;
+    if (tid >= (a.N - a.g0) * a.R2) return;
+    const long long g = a.g0 + tid / a.R2;
     const int r2 = (int)(tid % a.R2);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     if (a.accumulate) {
@@ -757,7 +757,7 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     {
         const char* env = std::getenv("REXP_LEAF");
         const bool want_dense = env && std::string(env) == "dense";
-        fdm = shared && model == REXP_MODEL_RSW && q <= FDM_T && !want_dense;
+        fdm = shared && model == REXP_MODEL_RSW && q <= SP_T && !want_dense;
     }
     store_bytes = 0;
     if (fdm) {
@@ -765,30 +765,39 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         for (int i = 0; i < q; ++i)
             for (int j = 0; j < q; ++j) K[static_cast<size_t>(i) * q + j] = ch.D2[(i + 1) * p + (j + 1)];
         if ((rc = real_eig(q, K, lam, V, Vi))) return rc;
-        std::vector<double> Vp(FDM_T * FDM_T, 0.0), Vip(FDM_T * FDM_T, 0.0);
+        std::vector<double> Vp(SP_T * SP_T, 0.0), Vip(SP_T * SP_T, 0.0);
         for (int i = 0; i < q; ++i)
             for (int j = 0; j < q; ++j) {
-                Vp[i * FDM_T + j] = V[static_cast<size_t>(i) * q + j];
-                Vip[i * FDM_T + j] = Vi[static_cast<size_t>(i) * q + j];
+                Vp[i * SP_T + j] = V[static_cast<size_t>(i) * q + j];
+                Vip[i * SP_T + j] = Vi[static_cast<size_t>(i) * q + j];
             }
         const double c2 = c1 * c1;
-        std::vector<double2> Dinv(static_cast<size_t>(nh) * FDM_T * FDM_T, make_double2(0.0, 0.0));
+        std::vector<double2> Dinv(static_cast<size_t>(nh) * SP_T * SP_T, make_double2(0.0, 0.0));
         for (int m = 0; m < nh; ++m) {
             const cd sg = pt.shift[h0 + m];
             for (int i = 0; i < q; ++i)
                 for (int j = 0; j < q; ++j) {
                     const cd v = 1.0 / (c2 * (lam[i] + lam[j]) - sg);
-                    Dinv[(static_cast<size_t>(m) * FDM_T + i) * FDM_T + j] = make_double2(v.real(), v.imag());
+                    Dinv[(static_cast<size_t>(m) * SP_T + i) * SP_T + j] = make_double2(v.real(), v.imag());
                 }
         }
         // e0 = V^T d_0, e1 = V^T d_{p-1}, d_r[k] = D[r][k+1]: the flux of the
         // particular solution in the spectral basis (UP pass)
-        std::vector<double> E01(2 * FDM_T, 0.0);
+        std::vector<double> E01(2 * SP_T, 0.0);
         for (int c = 0; c < q; ++c)
             for (int k = 0; k < q; ++k) {
                 E01[c] += V[static_cast<size_t>(k) * q + c] * ch.D[0 * p + k + 1];
-                E01[FDM_T + c] += V[static_cast<size_t>(k) * q + c] * ch.D[(p - 1) * p + k + 1];
+                E01[SP_T + c] += V[static_cast<size_t>(k) * q + c] * ch.D[(p - 1) * p + k + 1];
             }
+        // a0^ = V^-1 D2[1..q][0], a1^ = V^-1 D2[1..q][p-1]: the boundary coupling
+        // A_IB in the spectral basis (DOWN pass)
+        std::vector<double> A01(2 * SP_T, 0.0);
+        for (int ip = 0; ip < q; ++ip)
+            for (int i = 0; i < q; ++i) {
+                A01[ip] += Vi[static_cast<size_t>(ip) * q + i] * ch.D2[(i + 1) * p + 0];
+                A01[SP_T + ip] += Vi[static_cast<size_t>(ip) * q + i] * ch.D2[(i + 1) * p + (p - 1)];
+            }
+        if ((rc = put(&d_A01, A01))) return rc;
         if ((rc = put(&d_E01, E01))) return rc;
         if ((rc = put(&d_V, Vp))) return rc;
         if ((rc = put(&d_Vinv, Vip))) return rc;
@@ -803,6 +812,16 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     if ((rc = alloc(&d_Sleaf, static_cast<size_t>(nh) * pp_Sleaf))) return rc;
     store_bytes += static_cast<int64_t>(nh) * static_cast<int64_t>(pp_Ainv + pp_Sleaf) * 16;
     if ((rc = put(&d_leaf_gB, T.leaf_gB))) return rc;
+    {
+        // each edge node's pole sum is accumulated by the first leaf that contains it
+        std::vector<int32_t> own(T.leaf_gB.size(), 0);
+        std::vector<char> seen(static_cast<size_t>(NE), 0);
+        for (size_t b = 0; b < T.leaf_gB.size(); ++b) {
+            const int32_t ge = T.leaf_gB[b];
+            if (!seen[ge]) { seen[ge] = 1; own[b] = 1; }
+        }
+        if ((rc = put(&d_leaf_own, own))) return rc;
+    }
     levels.resize(T.levels.size());
     for (size_t li = 0; li < T.levels.size(); ++li) {
         const MergeLevel& L = T.levels[li];
@@ -837,12 +856,18 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     hstride = static_cast<long long>(hmax);
     size_t w3_per_pole = 0;
     for (auto& D : levels) w3_per_pole += static_cast<size_t>(D.nodes) * D.n3;
-    const size_t per_pole = (static_cast<size_t>(NI) + NE + 2 * hmax + w3_per_pole) * R2 * 16;
+    // the spectral leaf path never forms the per-pole interior solutions
+    const size_t per_pole = ((fdm ? 0 : static_cast<size_t>(NI)) + NE + 2 * hmax + w3_per_pole) * R2 * 16;
     {
         size_t budget = static_cast<size_t>(16) << 30;   // 16 GiB of per-pole work buffers
         const char* env = std::getenv("REXP_CHUNK");
         chunk = env ? std::max(1, std::atoi(env)) : static_cast<int>(std::max<size_t>(1, budget / per_pole));
         chunk = std::min(chunk, nh);
+    }
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     work_bytes = 0;
     auto walloc = [&](auto** pp, size_t count, size_t elt) -> int {
@@ -851,7 +876,17 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     };
     const size_t pc = static_cast<size_t>(chunk);
     if ((rc = walloc(&d_F, static_cast<size_t>(NI) * nF * R2, 8))) return rc;
-    if ((rc = walloc(&d_w, pc * NI * R2, 16))) return rc;
+    if (!fdm && (rc = walloc(&d_w, pc * NI * R2, 16))) return rc;
+    if (fdm) {
+        // pole groups per leaf CTA: enough CTAs to fill the GPU (REXP_GROUPS overrides)
+        const long long ctas = static_cast<long long>(nelem) * nrhs;
+        const char* env = std::getenv("REXP_GROUPS");
+        ngroups = env ? std::atoi(env) : static_cast<int>((16LL * num_sms + ctas - 1) / ctas);
+        ngroups = std::max(1, std::min(ngroups, chunk));
+        if ((rc = walloc(&d_G, static_cast<size_t>(nelem) * R2 * nF * q2, 8))) return rc;
+        if ((rc = walloc(&d_Ehat, static_cast<size_t>(ngroups) * nE * R2 * NI, 8))) return rc;
+        if ((rc = walloc(&d_Eedge, static_cast<size_t>(ngroups) * nE * R2 * NE, 8))) return rc;
+    }
     if ((rc = walloc(&d_edge, pc * NE * R2, 16))) return rc;
     if ((rc = walloc(&d_h[0], pc * hmax * R2, 16))) return rc;
     if ((rc = walloc(&d_h[1], pc * hmax * R2, 16))) return rc;
@@ -861,11 +896,6 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     }
     if ((rc = walloc(&d_E, static_cast<size_t>(nE) * R2 * N, 8))) return rc;
     if ((rc = walloc(&d_u, static_cast<size_t>(nrhs) * 3 * N * 2, 8))) return rc;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
     configure_kernels();
     return tune_stages(false);
 }
@@ -1001,8 +1031,6 @@ void cg_tile(int rows, int ncols, int& MT, int& WN, bool leaf = false) {
 
 void DeviceStore::configure_kernels() {
     cg_allow_all();
-    cudaFuncSetAttribute(k_leaf_fdm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_fdm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
     allow_all<4>();
@@ -1012,7 +1040,7 @@ void DeviceStore::configure_kernels() {
 int DeviceStore::launches_per_step() const {
     const int nchunks = (nh + chunk - 1) / chunk;
     const int per_chunk = (shared && !fdm ? 5 : 4) + 3 * static_cast<int>(levels.size());
-    return 2 + nchunks * per_chunk;
+    return fdm ? 4 + nchunks * (3 + 3 * static_cast<int>(levels.size())) : 2 + nchunks * per_chunk;
 }
 
 int DeviceStore::check(const char* what) {
@@ -1222,19 +1250,11 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     const int thr = ((q2 + 31) / 32) * 32;
     const int NBl = pick_nb(nelem, R2, shared);
     // ---- leaves up ----
-    FdmArgs fd{};
-    if (fdm) {
-        fd.E01 = d_E01; fd.V = d_V; fd.Vinv = d_Vinv; fd.Dinv = d_Dinv + static_cast<size_t>(m0) * FDM_T * FDM_T;
-        fd.D = d_D; fd.D2 = d_D2; fd.F = d_F; fd.cF = cF;
-        fd.q = q; fd.p = p; fd.nF = nF; fd.nelem = nelem; fd.R2 = R2; fd.nh = pc; fd.c1 = c1; fd.c2 = c1 * c1;
-        fd.h = d_h[0]; fd.hps = hstride; fd.edge = d_edge; fd.NE = NE; fd.gB = d_leaf_gB; fd.w = d_w;
-    }
-    const long long nprob = static_cast<long long>(pc) * nelem * R2;
-    const unsigned fdm_blocks = static_cast<unsigned>((nprob + FDM_WARPS - 1) / FDM_WARPS);
-    const size_t fdm_smem = (static_cast<size_t>(FDM_WARPS) * FDM_TILE_ELEMS + FDM_T * FDM_LDV) * sizeof(double2);
+    SpecArgs sp = spec_args(m0, pc);
+    const dim3 sp_grid(static_cast<unsigned>(nelem * nrhs), static_cast<unsigned>(sp.ngroups));
     if (fdm) {
         tbeg(s);
-        k_leaf_fdm<0><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
+        k_leaf_spec_up<<<sp_grid, SP_THREADS, 0, s>>>(sp);
         tend(T_LEAF_UP, s);
     } else if (shared) {
         CgemmArgs a{};
@@ -1287,7 +1307,7 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     // ---- leaves down ----
     if (fdm) {
         tbeg(s);
-        k_leaf_fdm<1><<<fdm_blocks, 32 * FDM_WARPS, fdm_smem, s>>>(fd);
+        k_leaf_spec_down<<<sp_grid, SP_THREADS, 0, s>>>(sp);
         tend(T_LEAF_DOWN, s);
     } else if (shared) {
         CgemmArgs a{};
@@ -1317,12 +1337,29 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     return check("tree_chunk");
 }
 
+SpecArgs DeviceStore::spec_args(int m0, int pc) const {
+    SpecArgs sp{};
+    sp.V = d_V; sp.Vinv = d_Vinv; sp.E01 = d_E01; sp.A01 = d_A01;
+    sp.Dinv = d_Dinv + static_cast<size_t>(m0) * SP_T * SP_T;
+    sp.cF = d_cF + static_cast<size_t>(m0) * nF;
+    sp.dE = d_dE + static_cast<size_t>(m0) * nE;
+    sp.F = d_F; sp.G = d_G;
+    sp.q = q; sp.p = p; sp.nF = nF; sp.nE = nE; sp.nelem = nelem; sp.R2 = R2; sp.nh = pc;
+    sp.ngroups = std::min(ngroups, pc); sp.accumulate = m0 > 0 ? 1 : 0;
+    sp.c1 = c1; sp.c2 = c1 * c1;
+    sp.h = d_h[0]; sp.hps = hstride;
+    sp.edge = d_edge; sp.NE = NE; sp.gB = d_leaf_gB; sp.own = d_leaf_own;
+    sp.Ehat = d_Ehat; sp.Eedge = d_Eedge; sp.E = nullptr; sp.N = N;
+    return sp;
+}
+
 int DeviceStore::pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s) {
     PoleSumArgs a{};
     a.accumulate = accumulate ? 1 : 0;
     a.w = d_w; a.edge = d_edge; a.dE = d_dE + static_cast<size_t>(m0) * nE; a.E = d_E_out;
     a.N = N; a.NI = NI; a.NE = NE; a.nh = pc; a.nE = nE; a.R2 = R2;
-    const long long tot = N * R2;
+    a.g0 = fdm ? NI : 0;   // spectral leaf path: interior sums come from k_spec_back
+    const long long tot = (N - a.g0) * R2;
     tbeg(s);
     k_pole_sum<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
     tend(T_POLE_SUM, s);
@@ -1339,11 +1376,25 @@ int DeviceStore::solve_sum(const double* d_state, double* d_E_out, cudaStream_t 
         k_pre<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
         tend(T_PRE, s);
     }
+    if (fdm) {
+        SpecArgs sp = spec_args(0, chunk);
+        tbeg(s);
+        k_spec_pre<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
+        tend(T_PRE, s);
+    }
     int rc;
     for (int m0 = 0; m0 < nh; m0 += chunk) {
         const int pc = std::min(chunk, nh - m0);
         if ((rc = tree_chunk(m0, pc, s))) return rc;
-        if ((rc = pole_sum_chunk(m0, pc, m0 > 0, d_E_out, s))) return rc;
+        if (!fdm && (rc = pole_sum_chunk(m0, pc, m0 > 0, d_E_out, s))) return rc;
+    }
+    if (fdm) {
+        SpecArgs sp = spec_args(0, chunk);
+        sp.E = d_E_out;
+        tbeg(s);
+        k_spec_back<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
+        tend(T_POLE_SUM, s);
+        return check("spec_back");
     }
     return REXP_OK;
 }

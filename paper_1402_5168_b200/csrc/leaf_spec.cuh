@@ -1,0 +1,390 @@
+// Spectral (tensor-product) leaf solves for the constant-coefficient (shared) store.
+//
+// On a leaf the interior collocation operator is a Kronecker sum
+//     A_II = c2 (I (x) K + K (x) I) - sigma_m,   K = D2[1..q][1..q],  c2 = (2/H)^2
+// (§2.2 collocation; interior index (i, j), i fastest).  With
+// K = V diag(l) V^-1 (real, kappa(V) ~ 1.6 for q <= 16):
+//     A_II^{-1} T = V W V^T,   W = (V^-1 T V^-T) ./ (c2 (l_i + l_j) - sigma_m).
+// Everything pole-dependent is elementwise in the spectral basis, so the
+// O(q^3) transforms are hoisted out of the pole loop:
+//   * RHS fields:   G_f = V^-1 F_f V^-T once per step (k_spec_pre), and
+//                   V^-1 (sum_f c_mf F_f) V^-T = sum_f c_mf G_f;
+//   * boundary:     A_IB u_B is a sum of four outer products a (x) u_side, so
+//                   V^-1 (A_IB u_B) V^-T = c2 (a0^ ul^T + a1^ ur^T + ub^ a0^T + ut^ a1^T)
+//                   with u^ = V^-1 u_side (q x q mat-vecs per pole);
+//   * pole sum:     V is real, so sum_m Re(d_mk V W_m V^T) = V [sum_m Re(d_mk W_m)] V^T:
+//                   the interior pole sums are accumulated in the spectral basis
+//                   and transformed back once per step (k_spec_back).
+//   UP:   h = N_I V W V^T (outward flux) from W through e_s = V^T d_s (four q-vectors).
+//   DOWN: E^_k += Re(d_mk W_m), the interior solutions u_m are never formed.
+// One CTA owns one (leaf, right-hand side) with both real parts and a
+// contiguous group of half poles; thread t < q^2 owns spectral mode
+// t = j' q + i'.
+#pragma once
+
+namespace rexp {
+namespace dev {
+
+constexpr int SP_T = 16;            // padded 1-D size of V, V^-1, Dinv rows
+constexpr int SP_THREADS = 256;     // >= q^2 for q <= 16
+constexpr int SP_PB = 4;            // half poles per batch (shared-memory staging)
+constexpr int SP_LW = SP_T + 1;     // stride of W tiles (odd: conflict-free row and column walks)
+constexpr int SP_NB = 4 * SP_T;     // max boundary nodes per leaf
+
+struct SpecArgs {
+    const double* V;        // 16 x 16 row-major, zero padded
+    const double* Vinv;     // 16 x 16 row-major, zero padded
+    const double* E01;      // e0 = V^T d_0, e1 = V^T d_{p-1} (d_r[k] = D[r][k+1]), 2 x 16
+    const double* A01;      // a0^ = V^-1 D2[1..q][0], a1^ = V^-1 D2[1..q][p-1], 2 x 16
+    const double2* Dinv;    // [nh][16*16] 1/(c2 (l_i + l_j) - sigma_m), (i', j') at i'*16 + j'
+    const double2* cF;      // [nh][nF]
+    const double2* dE;      // [nh][nE]
+    const double* F;        // [NI][nF][R2] pole-independent RHS fields (k_pre)
+    double* G;              // [nelem][R2][nF][q2] their spectral coefficients
+    int q, p, nF, nE, nelem, R2, nh, ngroups, accumulate;
+    double c1, c2;
+    // UP
+    double2* h;             // [nh][hps][R2]
+    long long hps;
+    // DOWN
+    const double2* edge;    // [nh][NE][R2]
+    long long NE;
+    const int* gB;          // [nelem][4q]
+    const int* own;         // [nelem][4q] 1 where this leaf owns the edge node's pole sum
+    double* Ehat;           // [ngroups][nE][R2][nelem * q2] spectral pole-sum partials
+    double* Eedge;          // [ngroups][nE][R2][NE] edge pole-sum partials
+    // BACK
+    double* E;              // [nE][R2][N]
+    long long N;
+};
+
+__device__ __forceinline__ void sp_group_range(const SpecArgs& a, int grp, int& m0, int& m1) {
+    const int base = a.nh / a.ngroups, rem = a.nh % a.ngroups;
+    m0 = grp * base + min(grp, rem);
+    m1 = m0 + base + (grp < rem ? 1 : 0);
+}
+
+// --------------------------------------------------------------------------
+// k_spec_pre: G_f = V^-1 F_f V^-T   (grid: nelem * R2 CTAs)
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(SP_THREADS) k_spec_pre(SpecArgs a) {
+    __shared__ double fs[3][SP_T * SP_T];
+    __shared__ double ts[3][SP_T * SP_T];
+    __shared__ double vis[SP_T * (SP_T + 1)];
+    const int q = a.q, q2 = q * q, t = threadIdx.x;
+    const int leaf = blockIdx.x / a.R2, r2 = blockIdx.x % a.R2;
+    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
+    for (int e = t; e < a.nF * q2; e += blockDim.x) {
+        const int f = e / q2, node = e % q2;   // node = j*q + i
+        fs[f][node] = a.F[(((size_t)leaf * q2 + node) * a.nF + f) * a.R2 + r2];
+    }
+    __syncthreads();
+    // T1[f][(j, i')] = sum_i Vinv[i'][i] F_f[i][j]
+    for (int e = t; e < a.nF * q2; e += blockDim.x) {
+        const int f = e / q2, node = e % q2, ip = node % q, j = node / q;
+        double s = 0.0;
+        for (int i = 0; i < q; ++i) s = fma(vis[ip * (SP_T + 1) + i], fs[f][j * q + i], s);
+        ts[f][j * q + ip] = s;
+    }
+    __syncthreads();
+    // G_f[(j', i')] = sum_j T1[f][(j, i')] Vinv[j'][j]
+    for (int e = t; e < a.nF * q2; e += blockDim.x) {
+        const int f = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
+        double s = 0.0;
+        for (int j = 0; j < q; ++j) s = fma(ts[f][j * q + ip], vis[jp * (SP_T + 1) + j], s);
+        a.G[(((size_t)leaf * a.R2 + r2) * a.nF + f) * q2 + mode] = s;
+    }
+}
+
+// the thread's spectral RHS coefficients G_f[mode] for both real parts of RHS k
+__device__ __forceinline__ void sp_load_g(const SpecArgs& a, int leaf, int k, int mode, double (&g)[2][3]) {
+    const int q2 = a.q * a.q;
+#pragma unroll
+    for (int part = 0; part < 2; ++part)
+#pragma unroll
+        for (int f = 0; f < 3; ++f)
+            g[part][f] = (f < a.nF) ? a.G[(((size_t)leaf * a.R2 + 2 * k + part) * a.nF + f) * q2 + mode] : 0.0;
+}
+
+// --------------------------------------------------------------------------
+// k_leaf_spec_up: h_m = N_I A_m^-1 f_m   (grid: nelem * nrhs, ngroups)
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
+    __shared__ double2 Ws[SP_PB][2][SP_T * SP_LW];  // W[i'][j'] at j'*SP_LW + i'
+    __shared__ double2 Ys[SP_PB][2][4][SP_T];       // y0, y1, z0, z1
+    __shared__ double vs[SP_T * (SP_T + 1)];
+    __shared__ double es[2 * SP_T];
+    const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
+    const int nrhs = a.R2 / 2;
+    const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
+    int m0, m1;
+    sp_group_range(a, blockIdx.y, m0, m1);
+    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
+    if (t < 2 * SP_T) es[t] = a.E01[t];
+    const bool act = t < q2;
+    const int ip = t % q, jp = t / q;
+    const int wpos = jp * SP_LW + ip;
+    double g[2][3];
+    if (act) sp_load_g(a, leaf, k, t, g);
+    __syncthreads();
+    for (int mb = m0; mb < m1; mb += SP_PB) {
+        const int nbat = min(SP_PB, m1 - mb);
+        // W = Dinv_m .* sum_f c_mf G_f
+        if (act) {
+#pragma unroll
+            for (int pp = 0; pp < SP_PB; ++pp) {
+                if (pp < nbat) {
+                    const int m = mb + pp;
+                    const double2* cf = a.cF + (size_t)m * a.nF;
+                    const double2 c0 = cf[0];
+                    const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0.0, 0.0);
+                    const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0.0, 0.0);
+                    const double2 d = __ldg(a.Dinv + (size_t)m * SP_T * SP_T + ip * SP_T + jp);
+#pragma unroll
+                    for (int part = 0; part < 2; ++part) {
+                        const double sx = c0.x * g[part][0] + c1v.x * g[part][1] + c2v.x * g[part][2];
+                        const double sy = c0.y * g[part][0] + c1v.y * g[part][1] + c2v.y * g[part][2];
+                        Ws[pp][part][wpos] = make_double2(sx * d.x - sy * d.y, sx * d.y + sy * d.x);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // rows:    y_s[i'] = sum_j' W[i'][j'] e_s[j']   (s = 0, 1 in one pass)
+        // columns: z_s[j'] = sum_i' W[i'][j'] e_s[i']
+        for (int task = t; task < nbat * 64; task += blockDim.x) {
+            const int pp = task >> 6, part = (task >> 5) & 1, col = (task >> 4) & 1, r = task & 15;
+            if (r >= q) continue;
+            const double2* W = Ws[pp][part];
+            const int base = col ? r * SP_LW : r, step = col ? 1 : SP_LW;
+            double s0x = 0.0, s0y = 0.0, s1x = 0.0, s1y = 0.0;
+            for (int c = 0; c < q; ++c) {
+                const double2 w = W[base + c * step];
+                const double e0 = es[c], e1 = es[SP_T + c];
+                s0x = fma(w.x, e0, s0x); s0y = fma(w.y, e0, s0y);
+                s1x = fma(w.x, e1, s1x); s1y = fma(w.y, e1, s1y);
+            }
+            Ys[pp][part][2 * col][r] = make_double2(s0x, s0y);
+            Ys[pp][part][2 * col + 1][r] = make_double2(s1x, s1y);
+        }
+        __syncthreads();
+        // bottom: -c1 V y0, right: +c1 V z1, top: +c1 V y1, left: -c1 V z0
+        for (int task = t; task < nbat * nbnd * 2; task += blockDim.x) {
+            const int pp = task / (2 * nbnd), rem = task % (2 * nbnd), b = rem >> 1, part = rem & 1;
+            const int side = b / q, s1 = b % q;
+            const int vec = side == 0 ? 0 : side == 1 ? 3 : side == 2 ? 1 : 2;
+            const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
+            const double2* y = Ys[pp][part][vec];
+            double sx = 0.0, sy = 0.0;
+            for (int kk = 0; kk < q; ++kk) {
+                const double v = vs[s1 * (SP_T + 1) + kk];
+                sx = fma(v, y[kk].x, sx);
+                sy = fma(v, y[kk].y, sy);
+            }
+            a.h[((size_t)(mb + pp) * a.hps + (size_t)leaf * nbnd + b) * a.R2 + 2 * k + part] =
+                make_double2(sgn * sx, sgn * sy);
+        }
+        // the next batch writes Ws (last read before the barrier above) and Ys
+        // (read here; its next writer runs after the next batch's first barrier)
+    }
+}
+
+// --------------------------------------------------------------------------
+// k_leaf_spec_down: E^_k += Re(d_mk W_m), W_m = Dinv_m .* V^-1 (f_m - A_IB u_B,m) V^-T,
+// plus the pole sums of the edge nodes this leaf owns   (grid: nelem * nrhs, ngroups)
+// --------------------------------------------------------------------------
+constexpr int SP_UBN = SP_PB * 2 * SP_NB;              // boundary values staged per batch
+constexpr int SP_UBR = (SP_UBN + SP_THREADS - 1) / SP_THREADS;
+
+__device__ __forceinline__ void sp_fetch_ub(const SpecArgs& a, const int* gb, int k, int mb, int nbat, int nbnd,
+                                            double2 (&r)[SP_UBR]) {
+#pragma unroll
+    for (int u = 0; u < SP_UBR; ++u) {
+        const int task = threadIdx.x + u * SP_THREADS;   // (pp, b, part), part fastest
+        const int pp = task / (2 * nbnd), rem = task % (2 * nbnd);
+        r[u] = make_double2(0.0, 0.0);
+        if (pp < nbat)
+            r[u] = a.edge[((size_t)(mb + pp) * a.NE + gb[rem >> 1]) * a.R2 + 2 * k + (rem & 1)];
+    }
+}
+
+__global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_down(SpecArgs a) {
+    __shared__ double2 UBs[2][SP_UBN];                  // boundary values [pp][b][part], double buffered
+    __shared__ double2 Us[SP_PB][2][4][SP_T];           // V^-1 u_side per pole, part, side
+    __shared__ double vis[SP_T * (SP_T + 1)];
+    __shared__ double as[2 * SP_T];
+    const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
+    const int nrhs = a.R2 / 2;
+    const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
+    const int grp = blockIdx.y;
+    int m0, m1;
+    sp_group_range(a, grp, m0, m1);
+    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
+    if (t < 2 * SP_T) as[t] = a.A01[t];
+    const bool act = t < q2;
+    const int ip = t % q, jp = t / q;
+    double g[2][3], Eacc[2][3];
+#pragma unroll
+    for (int part = 0; part < 2; ++part)
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) Eacc[part][kk] = 0.0;
+    const size_t NIs = (size_t)a.nelem * q2;
+    double* Eout = a.Ehat + (size_t)grp * a.nE * a.R2 * NIs + (size_t)leaf * q2 + t;
+    if (act) {
+        sp_load_g(a, leaf, k, t, g);
+        if (a.accumulate) {
+#pragma unroll
+            for (int part = 0; part < 2; ++part)
+#pragma unroll
+                for (int kk = 0; kk < 3; ++kk)
+                    if (kk < a.nE) Eacc[part][kk] = Eout[((size_t)kk * a.R2 + 2 * k + part) * NIs];
+        }
+    }
+    const int* gb = a.gB + (size_t)leaf * nbnd;
+    // edge pole sums: thread t < 2*nbnd owns (b, part) = (t/2, t%2) if the leaf owns node b
+    const bool eact = t < 2 * nbnd && a.own[(size_t)leaf * nbnd + (t >> 1)];
+    double Eg[3] = {0.0, 0.0, 0.0};
+    double* Eeout = nullptr;
+    if (eact) {
+        Eeout = a.Eedge + (size_t)grp * a.nE * a.R2 * a.NE + (size_t)(2 * k + (t & 1)) * a.NE + gb[t >> 1];
+        if (a.accumulate) {
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk)
+                if (kk < a.nE) Eg[kk] = Eeout[(size_t)kk * a.R2 * a.NE];
+        }
+    }
+    double2 pre[SP_UBR];
+    sp_fetch_ub(a, gb, k, m0, min(SP_PB, m1 - m0), nbnd, pre);
+#pragma unroll
+    for (int u = 0; u < SP_UBR; ++u) UBs[0][t + u * SP_THREADS] = pre[u];
+    __syncthreads();
+    const double c2 = a.c2;
+    int buf = 0;
+    for (int mb = m0; mb < m1; mb += SP_PB, buf ^= 1) {
+        const int nbat = min(SP_PB, m1 - mb);
+        // next batch's boundary values in flight while this batch computes
+        if (mb + SP_PB < m1) sp_fetch_ub(a, gb, k, mb + SP_PB, min(SP_PB, m1 - mb - SP_PB), nbnd, pre);
+        const double2* ub = UBs[buf];
+        // u^_side = V^-1 u_side  (boundary order: bottom (i), right (j), top (i), left (j))
+        for (int task = t; task < nbat * 128; task += blockDim.x) {
+            const int pp = task >> 7, part = (task >> 6) & 1, side = (task >> 4) & 3, r = task & 15;
+            if (r >= q) continue;
+            const double2* u = ub + pp * 2 * nbnd + 2 * side * q + part;
+            double sx = 0.0, sy = 0.0;
+            for (int j = 0; j < q; ++j) {
+                const double2 uv = u[2 * j];
+                const double v = vis[r * (SP_T + 1) + j];
+                sx = fma(v, uv.x, sx);
+                sy = fma(v, uv.y, sy);
+            }
+            Us[pp][part][side][r] = make_double2(sx, sy);
+        }
+        __syncthreads();
+        if (act) {
+            const double a0i = as[ip], a1i = as[SP_T + ip], a0j = as[jp], a1j = as[SP_T + jp];
+#pragma unroll
+            for (int pp = 0; pp < SP_PB; ++pp) {
+                if (pp < nbat) {
+                    const int m = mb + pp;
+                    const double2* cf = a.cF + (size_t)m * a.nF;
+                    const double2 c0 = cf[0];
+                    const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0.0, 0.0);
+                    const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0.0, 0.0);
+                    const double2 d = __ldg(a.Dinv + (size_t)m * SP_T * SP_T + ip * SP_T + jp);
+                    const double2* de = a.dE + (size_t)m * a.nE;
+                    const double2 d0 = de[0], d1 = de[1];
+                    const double2 d2 = a.nE > 2 ? de[2] : make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int part = 0; part < 2; ++part) {
+                        const double2 ubv = Us[pp][part][0][ip], ur = Us[pp][part][1][jp];
+                        const double2 ut = Us[pp][part][2][ip], ul = Us[pp][part][3][jp];
+                        const double bx = a0i * ul.x + a1i * ur.x + ubv.x * a0j + ut.x * a1j;
+                        const double by = a0i * ul.y + a1i * ur.y + ubv.y * a0j + ut.y * a1j;
+                        const double sx = c0.x * g[part][0] + c1v.x * g[part][1] + c2v.x * g[part][2] - c2 * bx;
+                        const double sy = c0.y * g[part][0] + c1v.y * g[part][1] + c2v.y * g[part][2] - c2 * by;
+                        const double wx = sx * d.x - sy * d.y, wy = sx * d.y + sy * d.x;
+                        Eacc[part][0] += d0.x * wx - d0.y * wy;
+                        Eacc[part][1] += d1.x * wx - d1.y * wy;
+                        Eacc[part][2] += d2.x * wx - d2.y * wy;
+                    }
+                }
+            }
+        }
+        if (eact) {
+            for (int pp = 0; pp < nbat; ++pp) {
+                const double2 u = ub[pp * 2 * nbnd + t];
+                const double2* de = a.dE + (size_t)(mb + pp) * a.nE;
+#pragma unroll
+                for (int kk = 0; kk < 3; ++kk)
+                    if (kk < a.nE) Eg[kk] += de[kk].x * u.x - de[kk].y * u.y;
+            }
+        }
+        // stage the prefetched batch; Us and UBs[buf] are rewritten after the barrier
+        if (mb + SP_PB < m1) {
+#pragma unroll
+            for (int u = 0; u < SP_UBR; ++u) UBs[buf ^ 1][t + u * SP_THREADS] = pre[u];
+        }
+        __syncthreads();
+    }
+    if (act) {
+#pragma unroll
+        for (int part = 0; part < 2; ++part)
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk)
+                if (kk < a.nE) Eout[((size_t)kk * a.R2 + 2 * k + part) * NIs] = Eacc[part][kk];
+    }
+    if (eact) {
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk)
+            if (kk < a.nE) Eeout[(size_t)kk * a.R2 * a.NE] = Eg[kk];
+    }
+}
+
+// --------------------------------------------------------------------------
+// k_spec_back: interior E_k = V (sum_groups E^_k) V^T and the owned edge nodes'
+// sums over groups   (grid: nelem * R2 CTAs)
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
+    __shared__ double es[3][SP_T * SP_T];
+    __shared__ double ts[3][SP_T * SP_T];
+    __shared__ double vs[SP_T * (SP_T + 1)];
+    const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
+    const int leaf = blockIdx.x / a.R2, r2 = blockIdx.x % a.R2;
+    const size_t NIs = (size_t)a.nelem * q2;
+    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
+    for (int e = t; e < a.nE * q2; e += blockDim.x) {
+        const int kk = e / q2, mode = e % q2;
+        const double* src = a.Ehat + ((size_t)kk * a.R2 + r2) * NIs + (size_t)leaf * q2 + mode;
+        double s = 0.0;
+        for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.R2 * NIs];
+        es[kk][mode] = s;   // E^[i'][j'] at j'*q + i'
+    }
+    for (int e = t; e < a.nE * nbnd; e += blockDim.x) {
+        const int kk = e / nbnd, b = e % nbnd;
+        if (!a.own[(size_t)leaf * nbnd + b]) continue;
+        const int ge = a.gB[(size_t)leaf * nbnd + b];
+        const double* src = a.Eedge + ((size_t)kk * a.R2 + r2) * a.NE + ge;
+        double s = 0.0;
+        for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.R2 * a.NE];
+        a.E[((size_t)kk * a.R2 + r2) * a.N + (a.N - a.NE) + ge] = s;
+    }
+    __syncthreads();
+    // T1[(j', i)] = sum_i' V[i][i'] E^[i'][j']
+    for (int e = t; e < a.nE * q2; e += blockDim.x) {
+        const int kk = e / q2, node = e % q2, i = node % q, jp = node / q;
+        double s = 0.0;
+        for (int ipp = 0; ipp < q; ++ipp) s = fma(vs[i * (SP_T + 1) + ipp], es[kk][jp * q + ipp], s);
+        ts[kk][jp * q + i] = s;
+    }
+    __syncthreads();
+    // E[i][j] = sum_j' T1[(j', i)] V[j][j']
+    for (int e = t; e < a.nE * q2; e += blockDim.x) {
+        const int kk = e / q2, node = e % q2, i = node % q, j = node / q;
+        double s = 0.0;
+        for (int jpp = 0; jpp < q; ++jpp) s = fma(ts[kk][jpp * q + i], vs[j * (SP_T + 1) + jpp], s);
+        a.E[((size_t)kk * a.R2 + r2) * a.N + (size_t)leaf * q2 + node] = s;
+    }
+}
+
+}  // namespace dev
+}  // namespace rexp

@@ -24,6 +24,8 @@ struct Level {
     size_t ppX = 0, ppY = 0, ppS = 0;                   // per-pole operator sizes (complex)
 };
 
+struct SpecArgs;
+
 class DeviceStore {
   public:
     ~DeviceStore();
@@ -76,7 +78,10 @@ class DeviceStore {
     double *d_D = nullptr, *d_Dw = nullptr, *d_kappa = nullptr, *d_NI = nullptr, *d_F = nullptr;
     int *d_elem_g = nullptr, *d_leaf_gB = nullptr, *d_rpos1 = nullptr, *d_rpos2 = nullptr, *d_rgs = nullptr;
     double2 *d_cF = nullptr, *d_dE = nullptr, *d_Dinv = nullptr;
-    double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_E01 = nullptr;
+    double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_E01 = nullptr, *d_A01 = nullptr;
+    double *d_G = nullptr, *d_Ehat = nullptr, *d_Eedge = nullptr;   // spectral RHS fields, pole-sum partials
+    int* d_leaf_own = nullptr;                  // [nelem][4q] edge-node ownership for the pole sums
+    int ngroups = 1;                            // pole groups per leaf CTA (spectral path)
     int chunk = 1;             // half poles per work-buffer chunk
     int num_sms = 148;
     size_t pp_Ainv = 0, pp_Sleaf = 0, pp_Xroot = 0;
@@ -89,6 +94,7 @@ class DeviceStore {
     private:
     std::vector<StageCfg> t_upx, t_upy, t_down;
     StageCfg t_root;
+    SpecArgs spec_args(int m0, int pc) const;
     int pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s);
     double2 *d_Ainv = nullptr, *d_Sleaf = nullptr, *d_Xroot = nullptr;
     double2 *d_w = nullptr, *d_edge = nullptr;
