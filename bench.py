@@ -112,36 +112,44 @@ def tree_dims(n, q):
     return out
 
 
-def class_work(cfg, nh, R2, shared, leaf="dense"):
+def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
     """Algorithmic FP64 flops and operator bytes per step, per kernel class.
-    Complex multiply-add = 8 flops; operator element = 16 bytes.  leaf = "tensor":
-    four q x q x q real-by-complex products per leaf solve (16 q^3 flops), plus the
-    flux (UP) or the boundary lift (DOWN)."""
+    Complex multiply-add = 8 flops, complex x real multiply-add = 4, complex
+    product = 6; operator element = 16 bytes.  leaf = "spectral" counts the
+    per-pole work of the spectral leaf kernels, per (half pole, leaf, real part):
+      UP:   W = Dinv .* sum_f c_f G_f   q^2 (4 nF + 6)
+            y_s, z_s (4 weighted row/column sums)            16 q^2
+            h = +-c1 V y (4 sides)                            16 q^2
+      DOWN: u^ = V^-1 u_side (4 sides)                        16 q^2
+            RHS + boundary outer products + Dinv + pole sums  q^2 (4 nF + 20 + 6 + 4 nE)
+            owned edge nodes' pole sums                       2q * 4 nE
+    The once-per-step transforms (k_spec_pre, k_spec_back) are O(q^3) per leaf,
+    not per pole, and are counted under pre / pole_sum."""
     n, q = cfg["n"], cfg["p"] - 2
     q2, e = q * q, n * n
     lv = tree_dims(n, q)
     per = lambda nodes: 1 if shared else nodes
-    if leaf == "tensor":
-        tensor_fl = nh * e * R2 * (16 * q ** 3)
-        return {
-            "leaf_up": (tensor_fl + nh * e * R2 * 4 * q * q * 4, nh * q * q * 16),
-            "leaf_down": (tensor_fl + nh * e * R2 * q2 * 4 * 2, nh * q * q * 16),
-            "merge_up": (sum(nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx in lv),
-                         sum(nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx in lv)),
-            "root": (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16),
-            "merge_down": (sum(nh * nd * n3 * nx * R2 * 8 for nd, n3, nx in lv),
-                           sum(nh * per(nd) * n3 * nx * 16 for nd, n3, nx in lv)),
-        }
-    w = {
-        "leaf_up": (nh * e * q2 * q2 * R2 * 8, nh * per(e) * q2 * q2 * 16),
-        "leaf_flux": (nh * e * 4 * q * q * R2 * 4, 0),
+    merge = {
         "merge_up": (sum(nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx in lv),
                      sum(nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx in lv)),
         "root": (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16),
         "merge_down": (sum(nh * nd * n3 * nx * R2 * 8 for nd, n3, nx in lv),
                        sum(nh * per(nd) * n3 * nx * 16 for nd, n3, nx in lv)),
+    }
+    if leaf == "spectral":
+        unit = nh * e * R2
+        w = {
+            "leaf_up": (unit * q2 * (4 * nF + 6 + 32), nh * q2 * 16),
+            "leaf_down": (unit * (16 * q2 + q2 * (4 * nF + 26 + 4 * nE) + 8 * q * nE), nh * q2 * 16),
+        }
+        w.update(merge)
+        return w
+    w = {
+        "leaf_up": (nh * e * q2 * q2 * R2 * 8, nh * per(e) * q2 * q2 * 16),
+        "leaf_flux": (nh * e * 4 * q * q * R2 * 4, 0),
         "leaf_down": (nh * e * q2 * 4 * q * R2 * 8, nh * per(e) * q2 * 4 * q * 16),
     }
+    w.update(merge)
     return w
 
 
@@ -152,14 +160,16 @@ def roofline_for(cfg, h, times, steps, pk):
     nh = h.num_half_poles
     R2 = 2 * h.nrhs
     shared = (cfg["model"] == "rsw")
-    work = class_work(cfg, nh, R2, shared, leaf=h.leaf_solver or "dense")
+    nF, nE = (3, 3) if cfg["model"] == "rsw" else (2, 2)
+    work = class_work(cfg, nh, R2, shared, leaf=h.leaf_solver or "dense", nF=nF, nE=nE)
     # dominant kernel = the single launch with the largest average duration
     # (the merge tree is many launches of different shapes; it is reported per class)
     dom = max((k for k in times if times[k][1]), key=lambda k: times[k][0] / times[k][1])
     ms, nl = times[dom]
     per_launch_ms = ms / max(nl, 1)
-    sm_max = pk.get("sm_max_mhz", 1965.0)
-    fp64_peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12      # 37.2 TFLOP/s; measured DMMA 37.2 (profiles/r01_fp64_peak.txt)
+    # the spectral leaf kernels run on the FP64 FMA pipe: measured DFMA 35.9 TFLOP/s
+    # (profiles/r01_fp64_peak.txt; nominal 148 SMs x 64 FMA/clk x 2 x 1965 MHz = 37.2)
+    fp64_peak = 35.93
     per_class = {}
     for k, (t, c) in times.items():
         if k in work and c:
@@ -177,7 +187,7 @@ def roofline_for(cfg, h, times, steps, pk):
         ach = fl / lps / (per_launch_ms * 1e-3) / 1e12
         return {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(fp64_peak, 2),
                 "unit": "TFLOP/s", "frac": round(ach / fp64_peak, 4), "traffic": traffic_for(dom),
-                "peak_source": "FP64 pipe 148 SMs x 64 FMA/clk x 2 x sm_max_mhz = 37.2 TF; measured DMMA 37.2 TF",
+                "peak_source": "measured DFMA 35.93 TF (profiles/r01_fp64_peak.txt, tools/fp64_peak.cu); nominal 37.2",
                 "per_launch_ms": round(per_launch_ms, 4), "per_class": per_class}
     hbm = pk.get("hbm_gbs", 6650.0)
     ach = by / lps / (per_launch_ms * 1e-3) / 1e9

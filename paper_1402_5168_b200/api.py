@@ -67,9 +67,11 @@ class Handle:
 
     @property
     def leaf_solver(self):
-        """'tensor' (tensor-product leaf inverse) or 'dense' (q^2 x q^2 leaf operators)."""
+        """'spectral' (tensor-product leaf inverse in the eigenbasis of the 1-D
+        second-derivative block, pole loop in the spectral basis) or 'dense'
+        (q^2 x q^2 leaf operators)."""
         v = int(_lib.load().rexp_leaf_solver(self.ptr))
-        return {0: "dense", 1: "tensor"}.get(v, None)
+        return {0: "dense", 1: "spectral"}.get(v, None)
 
     @property
     def stage_report(self):

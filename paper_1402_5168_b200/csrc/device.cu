@@ -675,11 +675,29 @@ int DeviceStore::timing_end(double* ms, int32_t* launches) {
         if (launches) launches[k] = 0;
     }
     if (!tlog.empty() && cudaEventSynchronize(tlog.back().b) != cudaSuccess) return check("timing_end");
-    for (auto& t : tlog) {
+    // REXP_TIMING_DETAIL=1: per-launch averages by position in the step (stderr)
+    const char* detail = std::getenv("REXP_TIMING_DETAIL");
+    const size_t lps = static_cast<size_t>(launches_per_step());
+    std::vector<double> pos_ms(detail ? lps : 0, 0.0);
+    std::vector<int> pos_cls(detail ? lps : 0, -1);
+    for (size_t i = 0; i < tlog.size(); ++i) {
+        const auto& t = tlog[i];
         float x = 0.f;
         cudaEventElapsedTime(&x, t.a, t.b);
         if (ms) ms[t.cls] += x;
         if (launches) launches[t.cls] += 1;
+        if (detail && lps) {
+            pos_ms[i % lps] += x;
+            pos_cls[i % lps] = t.cls;
+        }
+    }
+    if (detail && lps && tlog.size() >= lps) {
+        static const char* names[T_NCLASS] = {"pre", "leaf_up", "leaf_flux", "merge_up", "root",
+                                              "merge_down", "leaf_down", "pole_sum", "recover"};
+        const double nsteps = static_cast<double>(tlog.size() / lps);
+        for (size_t i = 0; i < lps; ++i)
+            std::fprintf(stderr, "launch %3zu %-10s %9.2f us\n", i, pos_cls[i] >= 0 ? names[pos_cls[i]] : "?",
+                         1e3 * pos_ms[i] / nsteps);
     }
     tlog.clear();
     tpool_used = 0;
