@@ -97,19 +97,24 @@ def make_problem(cfg, x, y):
 
 
 def tree_dims(n, q):
-    """(nodes, n3, next) of every merge level (x-merge first, alternating), as in mesh.cpp."""
+    """(nodes, n3, next) of every merge level (x-merge first, alternating), as in
+    mesh.cpp: the x-merge reaching the full width closes the periodic x seam too
+    (cylinder: n3 = both vertical seams, next = bottom + top)."""
     out = []
     ac = bc = 1
     lev = 0
-    while not (ac == n and bc == n):
+    while True:
         if lev % 2 == 0:
-            a, b, n3 = 2 * ac, bc, bc * q
+            a, b = 2 * ac, bc
+            if a == n:
+                out.append((n // b, 2 * bc * q, 2 * n * q))
+                return out
+            n3 = bc * q
         else:
             a, b, n3 = ac, 2 * bc, ac * q
         out.append(((n // a) * (n // b), n3, 2 * (a + b) * q))
         ac, bc = a, b
         lev += 1
-    return out
 
 
 def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):

@@ -108,10 +108,8 @@ __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int
         a.dst[(((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2] = v;
     } else if (MODE == CG_UPX) {
         a.dst[(size_t)m * a.dst_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2] = v;
-    } else if (MODE == CG_UPY) {
-        const double2 ad = a.add[((size_t)m * a.add_ps + a.ai0[(size_t)node * a.rows + row]) * R2 + r2];
-        a.dst[(size_t)m * a.dst_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2] =
-            make_double2(ad.x + v.x, ad.y + v.y);
+    } else if (MODE == CG_UPY) {   // additive child h[ext] folded in by the caller
+        a.dst[(size_t)m * a.dst_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2] = v;
     } else if (MODE == CG_ROOT) {   // seam values into the pole's edge array
         a.dst[((size_t)m * a.dst_ps + a.so0[row]) * R2 + r2] = v;
     } else {  // DOWN (additive w3 folded in by the caller)
@@ -191,8 +189,9 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
 #pragma unroll
         for (int n = 0; n < NTW; ++n) acc[i][n][0] = acc[i][n][1] = acc[i][n][2] = acc[i][n][3] = 0.0;
 
-    // additive epilogue terms (LEAF_DOWN: w, DOWN: w3) fetched before the K loop
-    constexpr bool kAdd = (MODE == CG_LEAF_DOWN || MODE == CG_DOWN);
+    // additive epilogue terms (LEAF_DOWN: w, DOWN: w3, UPY: child h[ext]) fetched
+    // before the K loop so their latency overlaps the products
+    constexpr bool kAdd = (MODE == CG_LEAF_DOWN || MODE == CG_DOWN || MODE == CG_UPY);
     double2 addv[kAdd ? MT : 1][kAdd ? NTW : 1][2];
     if (kAdd) {
 #pragma unroll
@@ -208,6 +207,8 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
                         const int node = col / R2, r2 = col % R2;
                         if (MODE == CG_LEAF_DOWN)
                             addv[i][n][j] = a.dst[(((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2];
+                        else if (MODE == CG_UPY)
+                            addv[i][n][j] = a.add[((size_t)m * a.add_ps + a.ai0[(size_t)node * a.rows + row]) * R2 + r2];
                         else
                             addv[i][n][j] = a.add[(size_t)m * a.add_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2];
                     }

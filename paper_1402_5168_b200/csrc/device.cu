@@ -860,7 +860,6 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         if ((rc = put(&D.g3, L.g3))) return rc;
     }
     ns = T.ns;
-    nroot_b = 4 * T.n * T.q;
     pp_Xroot = static_cast<size_t>(ns) * ns;
     if ((rc = alloc(&d_Xroot, nh * pp_Xroot))) return rc;
     store_bytes += static_cast<int64_t>(nh) * static_cast<int64_t>(pp_Xroot) * 16;

@@ -155,26 +155,46 @@ int build_tree(int n, int p, Tree& T) {
                 T.leaf_gB[static_cast<size_t>(e) * 4 * q + pos] = bg.gedge(ex, ey, 1, 1, pos);
         }
 
-    // merge levels
+    // merge levels.  Boxes alternate x- and y-merges; the x-merge that reaches the
+    // full width n closes the periodic x seam at the same time (both vertical
+    // interfaces, a.right|b.left and a.left|b.right), leaving a cylinder whose
+    // boundary is [bottom, top] only; the root then merges the two cylinders
+    // across both horizontal interfaces (DESIGN.md §6 "periodic closure").
     T.levels.clear();
     int ac = 1, bc = 1;
     int lev = 0;
-    while (!(ac == n && bc == n)) {
+    bool cylinder = false;
+    while (!cylinder) {
         MergeLevel L;
         L.dir = (lev % 2 == 0) ? 0 : 1;
         L.a = L.dir == 0 ? 2 * ac : ac;
         L.b = L.dir == 0 ? bc : 2 * bc;
+        cylinder = L.dir == 0 && L.a == n;
         L.nbx = n / L.a;
         L.nby = n / L.b;
         L.nodes = L.nbx * L.nby;
         L.nchild = 2 * (ac + bc) * q;
         L.child_nodes = (n / ac) * (n / bc);
-        L.next = 2 * (L.a + L.b) * q;
+        L.next = cylinder ? 2 * L.a * q : 2 * (L.a + L.b) * q;
         const int cbx = n / ac;  // child boxes per row
         // child boundary offsets
         const int c_bot = 0, c_right = ac * q, c_top = (ac + bc) * q, c_left = (2 * ac + bc) * q;
         std::vector<std::pair<int, int>> order;  // parent position -> (child 0/1, child pos)
-        if (L.dir == 0) {
+        if (cylinder) {
+            L.n3 = 2 * bc * q;
+            for (int t = 0; t < bc * q; ++t) {      // middle seam
+                L.ia3_pos.push_back(c_right + t);
+                L.ib3_pos.push_back(c_left + t);
+            }
+            for (int t = 0; t < bc * q; ++t) {      // periodic x seam
+                L.ia3_pos.push_back(c_left + t);
+                L.ib3_pos.push_back(c_right + t);
+            }
+            for (int t = 0; t < ac * q; ++t) order.push_back({0, c_bot + t});
+            for (int t = 0; t < ac * q; ++t) order.push_back({1, c_bot + t});
+            for (int t = 0; t < ac * q; ++t) order.push_back({0, c_top + t});
+            for (int t = 0; t < ac * q; ++t) order.push_back({1, c_top + t});
+        } else if (L.dir == 0) {
             L.n3 = bc * q;
             for (int t = 0; t < L.n3; ++t) {
                 L.ia3_pos.push_back(c_right + t);
@@ -239,7 +259,9 @@ int build_tree(int n, int p, Tree& T) {
                     L.ext[o] = (c == 0 ? ca : cb) * L.nchild + cpos;
                     L.ext_is_b[o] = c;
                     L.ext_pos[o] = cpos;
-                    L.gext[o] = bg.gedge(x0, y0, L.a, L.b, r);
+                    // cylinder boundary [bottom, top]: skip the box's right side
+                    const int bpos = (cylinder && r >= L.a * q) ? r + L.b * q : r;
+                    L.gext[o] = bg.gedge(x0, y0, L.a, L.b, bpos);
                     const int cx0 = (c == 0 ? ca_x : cb_x) * ac, cy0 = (c == 0 ? ca_y : cb_y) * bc;
                     if (bg.gedge(cx0, cy0, ac, bc, cpos) != L.gext[o]) {
                         set_error("internal: parent/child boundary mismatch");
@@ -252,21 +274,29 @@ int build_tree(int n, int p, Tree& T) {
         bc = T.levels.back().b;
         ++lev;
     }
-    // root closure (periodic seams)
+    // root: cylinder 0 (y0 = 0) and cylinder 1 (y0 = n/2) meet on the middle seam
+    // (0.top | 1.bottom) and the periodic y seam (0.bottom | 1.top); positions are
+    // flat indices into the cylinder level's boundary array, pos1 in cylinder 0
+    // and pos2 in cylinder 1
+    const MergeLevel& C = T.levels.back();
+    if (C.nodes != 2 || C.next != 2 * n * q) {
+        set_error("internal: cylinder level shape");
+        return REXP_EINVAL;
+    }
     const int nq = n * q;
     T.ns = 2 * nq;
     T.root_pos1.resize(T.ns);
     T.root_pos2.resize(T.ns);
     T.root_gs.resize(T.ns);
     for (int t = 0; t < nq; ++t) {
-        T.root_pos1[t] = t;                 // bottom
-        T.root_pos2[t] = 2 * nq + t;        // top
-        T.root_pos1[nq + t] = nq + t;       // right
-        T.root_pos2[nq + t] = 3 * nq + t;   // left
+        T.root_pos1[t] = nq + t;                // cylinder 0 top
+        T.root_pos2[t] = C.next + t;            // cylinder 1 bottom
+        T.root_pos1[nq + t] = t;                // cylinder 0 bottom
+        T.root_pos2[nq + t] = C.next + nq + t;  // cylinder 1 top
     }
     for (int s = 0; s < T.ns; ++s) {
-        T.root_gs[s] = bg.gedge(0, 0, n, n, T.root_pos1[s]);
-        if (bg.gedge(0, 0, n, n, T.root_pos2[s]) != T.root_gs[s]) {
+        T.root_gs[s] = C.gext[T.root_pos1[s]];
+        if (C.gext[T.root_pos2[s]] != T.root_gs[s]) {
             set_error("internal: periodic seam mismatch");
             return REXP_EINVAL;
         }

@@ -47,7 +47,7 @@ class DeviceStore {
 
     int model = 0, n = 0, p = 0, q = 0, q2 = 0, nb = 0, nelem = 0;
     long long N = 0, NI = 0, NV = 0, NE = 0;
-    int h0 = 0, h1 = 0, nh = 0, nrhs = 1, R2 = 2, nF = 0, nE = 0, ns = 0, nroot_b = 0;
+    int h0 = 0, h1 = 0, nh = 0, nrhs = 1, R2 = 2, nF = 0, nE = 0, ns = 0;
     bool shared = true;
     bool fdm = false;          // tensor-product leaf inverse (constant coefficients)
     double c1 = 0.0;

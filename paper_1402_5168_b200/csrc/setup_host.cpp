@@ -345,20 +345,20 @@ int factor_one(const Ctx& C, int hidx) {
         Tchild.swap(Tpar);
     }
 
-    // ---- root closure ----
+    // ---- root closure: the two cylinders merged across both horizontal seams ----
+    //   X = -(T^a_33 + T^b_33)^{-1},  s = X (h^a_3 + h^b_3)  (no exterior left)
     {
         const int ns = T.ns;
-        const int nroot = 4 * T.n * T.q;
-        const cd* Tr = Tchild[0].data();
+        const int nbc = T.levels.back().next;   // cylinder boundary size
+        const cd* Ta = Tchild[0].data();
+        const cd* Tb = Tchild[C.shared ? 0 : 1].data();
         std::vector<cd> X(static_cast<size_t>(ns) * ns);
         for (int a = 0; a < ns; ++a)
             for (int b = 0; b < ns; ++b) {
-                const int pa[2] = {T.root_pos1[a], T.root_pos2[a]};
-                const int pb[2] = {T.root_pos1[b], T.root_pos2[b]};
-                cd v = 0.0;
-                for (int u = 0; u < 2; ++u)
-                    for (int w = 0; w < 2; ++w) v += Tr[static_cast<size_t>(pa[u]) * nroot + pb[w]];
-                X[static_cast<size_t>(a) * ns + b] = v;
+                const int a1 = T.root_pos1[a], b1 = T.root_pos1[b];
+                const int a2 = T.root_pos2[a] - nbc, b2 = T.root_pos2[b] - nbc;
+                X[static_cast<size_t>(a) * ns + b] = Ta[static_cast<size_t>(a1) * nbc + b1] +
+                                                     Tb[static_cast<size_t>(a2) * nbc + b2];
             }
         if (!zinverse(ns, X.data())) {
             set_error("singular periodic closure (half pole " + std::to_string(hidx) + ")");
