@@ -384,6 +384,88 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
 }
 
 // --------------------------------------------------------------------------
+// k_root_fourier: periodic closure of the shared store in Fourier space.
+// The seam operator is block circulant in the element index e along x
+// (setup_host.cpp): s = X (h^a_3 + h^b_3) is applied as
+//   v^_k = sum_e v_e w^{-ke},  s^_k = X^_k v^_k,  s_e = (1/n) sum_k s^_k w^{ke}
+// with seam index (sigma, e, i) -> sigma n q + e q + i and r = sigma q + i.
+// grid: (ceil(R2 / RC), half poles); one CTA owns RC real right-hand sides.
+// --------------------------------------------------------------------------
+struct RootFArgs {
+    const double2* Xhat;    // [nh][n][2q x 2q] column-major blocks
+    const double2* h;       // cylinder-level boundary data [nh][hps][R2]
+    long long hps;
+    const int *pos1, *pos2, *gs;
+    double2* edge;          // [nh][NE][R2]
+    long long NE;
+    int n, q, R2, RC;
+};
+
+__global__ void __launch_bounds__(256) k_root_fourier(RootFArgs a) {
+    extern __shared__ double2 sm[];
+    const int m = blockIdx.y, c0 = blockIdx.x * a.RC;
+    const int n = a.n, q = a.q, r2q = 2 * q, nq = n * q, ns = 2 * nq, RC = a.RC;
+    const int nc = min(RC, a.R2 - c0);
+    double2* v = sm;                      // [ns][RC] seam sums, later s^ as [k][r][RC]
+    double2* vh = sm + (size_t)ns * RC;   // [k][r][RC]
+    double2* tw = vh + (size_t)ns * RC;   // w^j, j < n
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        double sn, cs;
+        sincospi(2.0 * j / n, &sn, &cs);
+        tw[j] = make_double2(cs, sn);
+    }
+    const double2* hm = a.h + (size_t)m * a.hps * a.R2;
+    for (int idx = threadIdx.x; idx < ns * RC; idx += blockDim.x) {
+        const int s = idx / RC, c = idx % RC;
+        double2 val = make_double2(0.0, 0.0);
+        if (c < nc) {
+            const double2 x = hm[(size_t)a.pos1[s] * a.R2 + c0 + c], y = hm[(size_t)a.pos2[s] * a.R2 + c0 + c];
+            val = make_double2(x.x + y.x, x.y + y.y);
+        }
+        v[idx] = val;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < ns * RC; idx += blockDim.x) {
+        const int c = idx % RC, r = (idx / RC) % r2q, k = idx / (RC * r2q);
+        const int sg = r / q, i = r % q;
+        double sx = 0.0, sy = 0.0;
+        for (int e = 0; e < n; ++e) {
+            const double2 w = tw[(k * e) % n];
+            const double2 x = v[((size_t)sg * nq + e * q + i) * RC + c];
+            sx += x.x * w.x + x.y * w.y;    // x conj(w)
+            sy += x.y * w.x - x.x * w.y;
+        }
+        vh[idx] = make_double2(sx, sy);
+    }
+    __syncthreads();
+    const double2* Xm = a.Xhat + (size_t)m * n * r2q * r2q;
+    for (int idx = threadIdx.x; idx < ns * RC; idx += blockDim.x) {
+        const int c = idx % RC, r = (idx / RC) % r2q, k = idx / (RC * r2q);
+        const double2* X = Xm + (size_t)k * r2q * r2q + r;
+        const double2* x = vh + (size_t)k * r2q * RC + c;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int rp = 0; rp < r2q; ++rp) cfma(acc, ldg2(X + (size_t)rp * r2q), x[rp * RC]);
+        v[idx] = acc;
+    }
+    __syncthreads();
+    const double inv = 1.0 / n;
+    double2* em = a.edge + (size_t)m * a.NE * a.R2;
+    for (int idx = threadIdx.x; idx < ns * RC; idx += blockDim.x) {
+        const int c = idx % RC, s = idx / RC;
+        if (c >= nc) continue;
+        const int sg = s / nq, e = (s % nq) / q, i = s % q, r = sg * q + i;
+        double sx = 0.0, sy = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const double2 w = tw[(k * e) % n];
+            const double2 x = v[((size_t)k * r2q + r) * RC + c];
+            sx += x.x * w.x - x.y * w.y;
+            sy += x.x * w.y + x.y * w.x;
+        }
+        em[(size_t)a.gs[s] * a.R2 + c0 + c] = make_double2(sx * inv, sy * inv);
+    }
+}
+
+// --------------------------------------------------------------------------
 // k_leaf_down<R2, NB>: u_I = w + S_leaf u_B (in place over w)
 // --------------------------------------------------------------------------
 struct LeafDownArgs {
@@ -860,7 +942,8 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         if ((rc = put(&D.g3, L.g3))) return rc;
     }
     ns = T.ns;
-    pp_Xroot = static_cast<size_t>(ns) * ns;
+    // shared store: n Fourier blocks of the block-circulant seam operator
+    pp_Xroot = shared ? static_cast<size_t>(T.n) * 4 * T.q * T.q : static_cast<size_t>(ns) * ns;
     if ((rc = alloc(&d_Xroot, nh * pp_Xroot))) return rc;
     store_bytes += static_cast<int64_t>(nh) * static_cast<int64_t>(pp_Xroot) * 16;
     if ((rc = put(&d_rpos1, T.root_pos1))) return rc;
@@ -941,7 +1024,7 @@ int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
         if ((rc = up(ops[li + 1].m[1], D.Y, D.ppY))) return rc;
         if ((rc = up(ops[li + 1].m[2], D.S, D.ppS))) return rc;
     }
-    return up(ops.back().m[0], d_Xroot, pp_Xroot);
+    return up(ops.back().m[shared ? 1 : 0], d_Xroot, pp_Xroot);
 }
 
 // launch helpers -------------------------------------------------------------
@@ -1049,6 +1132,7 @@ void cg_tile(int rows, int ncols, int& MT, int& WN, bool leaf = false) {
 void DeviceStore::configure_kernels() {
     cg_allow_all();
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
@@ -1078,6 +1162,16 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     if (kind == 3) {
         const double2* hr = d_h[levels.size() % 2];
         const double2* Xr = d_Xroot + static_cast<size_t>(m0) * pp_Xroot;
+        if (shared) {
+            RootFArgs a{};
+            a.Xhat = Xr; a.h = hr; a.hps = hstride; a.pos1 = d_rpos1; a.pos2 = d_rpos2; a.gs = d_rgs;
+            a.edge = d_edge; a.NE = NE; a.n = n; a.q = q; a.R2 = R2; a.RC = std::min(R2, 4);
+            const size_t smem = (2 * static_cast<size_t>(ns) * a.RC + n) * sizeof(double2);
+            tbeg(s);
+            k_root_fourier<<<dim3((R2 + a.RC - 1) / a.RC, pc), 256, smem, s>>>(a);
+            tend(T_ROOT, s);
+            return REXP_OK;
+        }
         if (cfg.kind == 0) {
             CgemmArgs a{};
             a.A = Xr; a.rows = ns; a.K = ns; a.nodes = 1; a.R2 = R2;
@@ -1240,7 +1334,7 @@ int DeviceStore::tune_stages(bool measure) {
         tune(1, li, t_upy[li]);
         tune(2, li, t_down[li]);
     }
-    tune(3, 0, t_root);
+    if (!shared) tune(3, 0, t_root);
     timing = saved_timing;
     tuned = true;
     if (flush) cudaFree(flush);
@@ -1257,7 +1351,7 @@ std::string DeviceStore::stage_report() const {
     std::string s = tuned ? "tuned:" : "default:";
     for (size_t li = 0; li < levels.size(); ++li)
         s += " L" + std::to_string(li + 1) + "[" + one(t_upx[li]) + "," + one(t_upy[li]) + "," + one(t_down[li]) + "]";
-    s += " root[" + one(t_root) + "]";
+    s += shared ? std::string(" root[fourier]") : " root[" + one(t_root) + "]";
     return s;
 }
 

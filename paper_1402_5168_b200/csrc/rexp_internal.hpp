@@ -116,7 +116,9 @@ int real_eig(int q, const std::vector<double>& K, std::vector<double>& lam, std:
              std::vector<double>& Vinv);
 
 // Host HPS factorization of half poles [h0, h1) into ops (levels: 0 leaf, 1..L merges, L+1 root)
+// root_fourier (shared store only): the periodic closure as n Fourier blocks
+// (ops.back().m[1], [half][n][2q x 2q]) instead of the dense ns x ns inverse (m[0])
 int factor_host(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1,
-                bool shared, int nthreads, std::vector<HostLevelOps>& ops);
+                bool shared, int nthreads, std::vector<HostLevelOps>& ops, bool root_fourier = false);
 
 }  // namespace rexp

@@ -241,6 +241,7 @@ struct Ctx {
     const PoleTables* pt;
     LeafGeom lg;
     bool shared;
+    bool root_fourier;
     int h0;
     std::vector<HostLevelOps>* ops;
 };
@@ -352,21 +353,58 @@ int factor_one(const Ctx& C, int hidx) {
         const int nbc = T.levels.back().next;   // cylinder boundary size
         const cd* Ta = Tchild[0].data();
         const cd* Tb = Tchild[C.shared ? 0 : 1].data();
-        std::vector<cd> X(static_cast<size_t>(ns) * ns);
+        std::vector<cd> M(static_cast<size_t>(ns) * ns);
         for (int a = 0; a < ns; ++a)
             for (int b = 0; b < ns; ++b) {
                 const int a1 = T.root_pos1[a], b1 = T.root_pos1[b];
                 const int a2 = T.root_pos2[a] - nbc, b2 = T.root_pos2[b] - nbc;
-                X[static_cast<size_t>(a) * ns + b] = Ta[static_cast<size_t>(a1) * nbc + b1] +
+                M[static_cast<size_t>(a) * ns + b] = Ta[static_cast<size_t>(a1) * nbc + b1] +
                                                      Tb[static_cast<size_t>(a2) * nbc + b2];
             }
-        if (!zinverse(ns, X.data())) {
-            set_error("singular periodic closure (half pole " + std::to_string(hidx) + ")");
-            return REXP_ESINGULAR;
-        }
-        for (auto& v : X) v = -v;
         HostLevelOps& LR = ops.back();
-        store_colmajor(X.data(), ns, ns, LR.m[0].data() + static_cast<size_t>(slot) * ns * ns);
+        if (C.root_fourier) {
+            // Translation invariance along x (shared store): seam index s = (sigma, e, i)
+            // = sigma*n*q + e*q + i, and M[(sigma,e,i),(sigma',e',i')] depends on e - e'
+            // only, so M is block circulant:  C_d = M[(., e'+d, .), (., e', .)]
+            // (averaged over e'),  M^_k = sum_d C_d w^{-kd},  w = exp(2 pi i / n),
+            // and X^_k = -(M^_k)^{-1}   (DESIGN.md §6 "Fourier root").
+            const int n = T.n, q = T.q, r2q = 2 * q, nq = n * q;
+            auto sidx = [&](int sg, int e, int i) { return sg * nq + ((e % n + n) % n) * q + i; };
+            std::vector<cd> Cd(static_cast<size_t>(n) * r2q * r2q, cd(0.0));
+            for (int d = 0; d < n; ++d)
+                for (int ep = 0; ep < n; ++ep)
+                    for (int sg = 0; sg < 2; ++sg)
+                        for (int i = 0; i < q; ++i)
+                            for (int sg2 = 0; sg2 < 2; ++sg2)
+                                for (int i2 = 0; i2 < q; ++i2)
+                                    Cd[(static_cast<size_t>(d) * r2q + sg * q + i) * r2q + sg2 * q + i2] +=
+                                        M[static_cast<size_t>(sidx(sg, ep + d, i)) * ns + sidx(sg2, ep, i2)] /
+                                        static_cast<double>(n);
+            constexpr double kPi = 3.14159265358979323846;
+            std::vector<cd> Mk(static_cast<size_t>(r2q) * r2q);
+            for (int k = 0; k < n; ++k) {
+                std::fill(Mk.begin(), Mk.end(), cd(0.0));
+                for (int d = 0; d < n; ++d) {
+                    const double ang = -2.0 * kPi * static_cast<double>((static_cast<long long>(k) * d) % n) / n;
+                    const cd w(std::cos(ang), std::sin(ang));
+                    for (int e = 0; e < r2q * r2q; ++e) Mk[e] += Cd[static_cast<size_t>(d) * r2q * r2q + e] * w;
+                }
+                if (!zinverse(r2q, Mk.data())) {
+                    set_error("singular periodic closure block (half pole " + std::to_string(hidx) + ")");
+                    return REXP_ESINGULAR;
+                }
+                for (auto& v : Mk) v = -v;
+                store_colmajor(Mk.data(), r2q, r2q,
+                               LR.m[1].data() + (static_cast<size_t>(slot) * n + k) * r2q * r2q);
+            }
+        } else {
+            if (!zinverse(ns, M.data())) {
+                set_error("singular periodic closure (half pole " + std::to_string(hidx) + ")");
+                return REXP_ESINGULAR;
+            }
+            for (auto& v : M) v = -v;
+            store_colmajor(M.data(), ns, ns, LR.m[0].data() + static_cast<size_t>(slot) * ns * ns);
+        }
     }
     return REXP_OK;
 }
@@ -374,10 +412,11 @@ int factor_one(const Ctx& C, int hidx) {
 }  // namespace
 
 int factor_host(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1, bool shared,
-                int nthreads, std::vector<HostLevelOps>& ops) {
+                int nthreads, std::vector<HostLevelOps>& ops, bool root_fourier) {
     const int nh = h1 - h0;
     const Cheb ch = make_cheb(T.p);
-    Ctx C{&P, &T, &pt, make_leaf_geom(ch, T.n), shared, h0, &ops};
+    root_fourier = root_fourier && shared;
+    Ctx C{&P, &T, &pt, make_leaf_geom(ch, T.n), shared, root_fourier, h0, &ops};
     const int q2 = C.lg.q2, nb = C.lg.nb;
     // allocate
     ops.assign(T.levels.size() + 2, HostLevelOps());
@@ -405,8 +444,13 @@ int factor_host(const Problem& P, const Tree& T, const PoleTables& pt, int h0, i
         HostLevelOps& LR = ops.back();
         LR.nmat = 1;
         LR.nodes_stored = 1;
-        LR.rows[0] = T.ns; LR.cols[0] = T.ns;
-        LR.m[0].resize(static_cast<size_t>(nh) * T.ns * T.ns);
+        if (root_fourier) {   // n Fourier blocks of (2q x 2q)
+            LR.rows[1] = 2 * T.q; LR.cols[1] = 2 * T.q * T.n;
+            LR.m[1].resize(static_cast<size_t>(nh) * T.n * 4 * T.q * T.q);
+        } else {
+            LR.rows[0] = T.ns; LR.cols[0] = T.ns;
+            LR.m[0].resize(static_cast<size_t>(nh) * T.ns * T.ns);
+        }
     }
     if (nthreads <= 0) nthreads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     nthreads = std::min(nthreads, std::max(1, nh));

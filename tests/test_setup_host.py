@@ -204,3 +204,37 @@ def test_device_setup_fails_loudly_without_gpu():
     from paper_1402_5168_b200._lib import RexpError
     with pytest.raises(RexpError, match="CUDA|device"):
         api.setup("rsw", n=2, p=6, tau=0.2, delta=1e-10, Lambda=50.0, device=0)
+
+
+def test_root_seam_operator_block_circulant(host_rsw):
+    """DESIGN.md §6 "Fourier root": on the periodic mesh with constant
+    coefficients the root seam operator X = -(T^a_33 + T^b_33)^{-1} commutes
+    with translation by one element along x, i.e. it is block circulant in the
+    element index e of the seam index (sigma, e, i) = sigma n q + e q + i.  The
+    device store applies it through n Fourier blocks; this checks the premise on
+    the dense per-node root (computed without that assumption), and that the
+    Fourier blocks rebuild it."""
+    from paper_1402_5168_b200 import api
+    h = host_rsw
+    n, q = 4, 6
+    nlev = api.export_num_levels(h)
+    ns = api.export_level_info(h, nlev - 1)[2]
+    assert ns == 2 * n * q
+    for half in (0, h.num_half_poles // 2, h.num_half_poles - 1):
+        X = api.export_matrix(h, half, nlev - 1, 0, 0, ns, ns)
+        B = X.reshape(2, n, q, 2, n, q)
+        scale = np.abs(X).max()
+        for e in range(n):
+            for ep in range(n):
+                d = (e - ep) % n
+                assert np.abs(B[:, e, :, :, ep, :] - B[:, d, :, :, 0, :]).max() < 1e-11 * scale
+        # Fourier blocks X^_k = sum_d C_d w^{-kd}; inverse transform rebuilds X
+        C = np.stack([B[:, d, :, :, 0, :].reshape(2 * q, 2 * q) for d in range(n)])
+        w = np.exp(-2j * np.pi * np.outer(np.arange(n), np.arange(n)) / n)
+        Xh = np.einsum("kd,dab->kab", w, C)
+        Cb = np.einsum("kd,kab->dab", np.conj(w), Xh) / n
+        R = np.zeros((2, n, q, 2, n, q), complex)
+        for e in range(n):
+            for ep in range(n):
+                R[:, e, :, :, ep, :] = Cb[(e - ep) % n].reshape(2, q, 2, q)
+        assert np.abs(R.reshape(ns, ns) - X).max() < 1e-11 * scale
