@@ -401,7 +401,7 @@ struct RootFArgs {
     int n, q, R2, RC;
 };
 
-__global__ void __launch_bounds__(256) k_root_fourier(RootFArgs a) {
+__global__ void __launch_bounds__(1024) k_root_fourier(RootFArgs a) {
     extern __shared__ double2 sm[];
     const int m = blockIdx.y, c0 = blockIdx.x * a.RC;
     const int n = a.n, q = a.q, r2q = 2 * q, nq = n * q, ns = 2 * nq, RC = a.RC;
@@ -443,9 +443,18 @@ __global__ void __launch_bounds__(256) k_root_fourier(RootFArgs a) {
         const int c = idx % RC, r = (idx / RC) % r2q, k = idx / (RC * r2q);
         const double2* X = Xm + (size_t)k * r2q * r2q + r;
         const double2* x = vh + (size_t)k * r2q * RC + c;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int rp = 0; rp < r2q; ++rp) cfma(acc, ldg2(X + (size_t)rp * r2q), x[rp * RC]);
-        v[idx] = acc;
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int rp = 0;
+        for (; rp + 4 <= r2q; rp += 4) {
+            const double2 x0 = ldg2(X + (size_t)rp * r2q), x1 = ldg2(X + (size_t)(rp + 1) * r2q);
+            const double2 x2 = ldg2(X + (size_t)(rp + 2) * r2q), x3 = ldg2(X + (size_t)(rp + 3) * r2q);
+            cfma(acc0, x0, x[rp * RC]);
+            cfma(acc1, x1, x[(rp + 1) * RC]);
+            cfma(acc0, x2, x[(rp + 2) * RC]);
+            cfma(acc1, x3, x[(rp + 3) * RC]);
+        }
+        for (; rp < r2q; ++rp) cfma(acc0, ldg2(X + (size_t)rp * r2q), x[rp * RC]);
+        v[idx] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
     }
     __syncthreads();
     const double inv = 1.0 / n;
@@ -1167,8 +1176,9 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
             a.Xhat = Xr; a.h = hr; a.hps = hstride; a.pos1 = d_rpos1; a.pos2 = d_rpos2; a.gs = d_rgs;
             a.edge = d_edge; a.NE = NE; a.n = n; a.q = q; a.R2 = R2; a.RC = std::min(R2, 4);
             const size_t smem = (2 * static_cast<size_t>(ns) * a.RC + n) * sizeof(double2);
+            const int thr = std::min(1024, ((ns * a.RC + 31) / 32) * 32);   // one task per thread per phase
             tbeg(s);
-            k_root_fourier<<<dim3((R2 + a.RC - 1) / a.RC, pc), 256, smem, s>>>(a);
+            k_root_fourier<<<dim3((R2 + a.RC - 1) / a.RC, pc), thr, smem, s>>>(a);
             tend(T_ROOT, s);
             return REXP_OK;
         }
