@@ -126,8 +126,11 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
             y_s, z_s (4 weighted row/column sums)            16 q^2
             h = +-c1 V y (4 sides)                            16 q^2
       DOWN: u^ = V^-1 u_side (4 sides)                        16 q^2
-            RHS + boundary outer products + Dinv + pole sums  q^2 (4 nF + 20 + 6 + 4 nE)
+            boundary outer products b (4 complex x real)      16 q^2
+            t = -c2 Dinv b, pole sums Re(d_k t)               q^2 (8 + 4 nE)
             owned edge nodes' pole sums                       2q * 4 nE
+            (the RHS-field part of the pole sum is pole-independent,
+            sum_m Re(d_mk c_mf Dinv_m) =: Pi_kf, applied once per step in k_spec_back)
     The once-per-step transforms (k_spec_pre, k_spec_back) are O(q^3) per leaf,
     not per pole, and are counted under pre / pole_sum."""
     n, q = cfg["n"], cfg["p"] - 2
@@ -145,7 +148,7 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
         unit = nh * e * R2
         w = {
             "leaf_up": (unit * q2 * (4 * nF + 6 + 32), nh * q2 * 16),
-            "leaf_down": (unit * (16 * q2 + q2 * (4 * nF + 26 + 4 * nE) + 8 * q * nE), nh * q2 * 16),
+            "leaf_down": (unit * (32 * q2 + q2 * (8 + 4 * nE) + 8 * q * nE), nh * q2 * 16),
         }
         w.update(merge)
         return w

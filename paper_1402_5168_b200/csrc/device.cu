@@ -911,6 +911,21 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         if ((rc = put(&d_V, Vp))) return rc;
         if ((rc = put(&d_Vinv, Vip))) return rc;
         if ((rc = put(&d_Dinv, Dinv))) return rc;
+        // Pi_kf(i', j') = sum_m Re(d_mk c_mf Dinv_m(i', j')) over this handle's half poles:
+        // the pole sum of the RHS-field part of the interior solutions (k_spec_back)
+        {
+            std::vector<double> Pi(static_cast<size_t>(nE) * nF * SP_T * SP_T, 0.0);
+            for (int m = 0; m < nh; ++m)
+                for (int kk = 0; kk < nE; ++kk)
+                    for (int f = 0; f < nF; ++f) {
+                        const cd w = pt.dE[static_cast<size_t>(h0 + m) * nE + kk] * pt.cF[static_cast<size_t>(h0 + m) * nF + f];
+                        for (int e = 0; e < SP_T * SP_T; ++e) {
+                            const double2 dv = Dinv[static_cast<size_t>(m) * SP_T * SP_T + e];
+                            Pi[(static_cast<size_t>(kk) * nF + f) * SP_T * SP_T + e] += (w * cd(dv.x, dv.y)).real();
+                        }
+                    }
+            if ((rc = put(&d_Pi, Pi))) return rc;
+        }
         store_bytes += static_cast<int64_t>(Dinv.size()) * 16;
     }
     // operator store, filled by upload_ops (possibly in pole chunks)
@@ -1142,6 +1157,7 @@ void DeviceStore::configure_kernels() {
     cg_allow_all();
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_spec_down, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
@@ -1428,7 +1444,7 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     // ---- leaves down ----
     if (fdm) {
         tbeg(s);
-        k_leaf_spec_down<<<sp_grid, SP_THREADS, 0, s>>>(sp);
+        k_leaf_spec_down<<<sp_grid, SP_THREADS, sp_down_smem(), s>>>(sp);
         tend(T_LEAF_DOWN, s);
     } else if (shared) {
         CgemmArgs a{};
@@ -1470,7 +1486,7 @@ SpecArgs DeviceStore::spec_args(int m0, int pc) const {
     sp.c1 = c1; sp.c2 = c1 * c1;
     sp.h = d_h[0]; sp.hps = hstride;
     sp.edge = d_edge; sp.NE = NE; sp.gB = d_leaf_gB; sp.own = d_leaf_own;
-    sp.Ehat = d_Ehat; sp.Eedge = d_Eedge; sp.E = nullptr; sp.N = N;
+    sp.Ehat = d_Ehat; sp.Eedge = d_Eedge; sp.Pi = d_Pi; sp.E = nullptr; sp.N = N;
     return sp;
 }
 

@@ -52,6 +52,7 @@ struct SpecArgs {
     const int* gB;          // [nelem][4q]
     const int* own;         // [nelem][4q] 1 where this leaf owns the edge node's pole sum
     double* Ehat;           // [ngroups][nE][R2][nelem * q2] spectral pole-sum partials
+    const double* Pi;       // [nE][nF][16*16] sum_m Re(d_mk c_mf Dinv_m), (i', j') at i'*16 + j'
     double* Eedge;          // [ngroups][nE][R2][NE] edge pole-sum partials
     // BACK
     double* E;              // [nE][R2][N]
@@ -190,8 +191,16 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
 }
 
 // --------------------------------------------------------------------------
-// k_leaf_spec_down: E^_k += Re(d_mk W_m), W_m = Dinv_m .* V^-1 (f_m - A_IB u_B,m) V^-T,
-// plus the pole sums of the edge nodes this leaf owns   (grid: nelem * nrhs, ngroups)
+// k_leaf_spec_down: interior pole sums, boundary-driven part
+//   W_m = Dinv_m .* V^-1 (f_m - A_IB u_B,m) V^-T  and  E^_k = sum_m Re(d_mk W_m).
+// The f_m part is pole-independent up to a per-mode weight,
+//   sum_m Re(d_mk c_mf Dinv_m) =: Pi_kf   (setup, device.cu),
+// and is added once per step in k_spec_back; per pole only
+//   E^_k += Re((-c2 d_mk) Dinv_m .* b_m),  b_m = a0^ ul^T + a1^ ur^T + ub^ a0^T + ut^ a1^T
+// remains, plus the pole sums of the edge nodes this leaf owns.
+// Per batch of SP_PB half poles the boundary values (registers) and the Dinv
+// rows (cp.async) of the NEXT batch are in flight while this batch computes.
+//   (grid: nelem * nrhs, ngroups; dynamic shared memory sp_down_smem())
 // --------------------------------------------------------------------------
 constexpr int SP_UBN = SP_PB * 2 * SP_NB;              // boundary values staged per batch
 constexpr int SP_UBR = (SP_UBN + SP_THREADS - 1) / SP_THREADS;
@@ -208,37 +217,49 @@ __device__ __forceinline__ void sp_fetch_ub(const SpecArgs& a, const int* gb, in
     }
 }
 
-__global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_down(SpecArgs a) {
-    __shared__ double2 UBs[2][SP_UBN];                  // boundary values [pp][b][part], double buffered
-    __shared__ double2 Us[SP_PB][2][4][SP_T];           // V^-1 u_side per pole, part, side
-    __shared__ double vis[SP_T * (SP_T + 1)];
-    __shared__ double as[2 * SP_T];
+// Dinv rows of a batch: SP_PB x 256 complex, one 16-byte cp.async per thread per pole
+__device__ __forceinline__ void sp_fetch_dinv(const SpecArgs& a, int mb, int nbat, double2* dst) {
+    for (int pp = 0; pp < nbat; ++pp)
+        cp_async16(dst + pp * SP_T * SP_T + threadIdx.x, a.Dinv + (size_t)(mb + pp) * SP_T * SP_T + threadIdx.x);
+    cp_async_commit();
+}
+
+constexpr size_t sp_down_smem() {
+    return (2 * (size_t)SP_UBN + (size_t)SP_PB * 2 * 4 * SP_T + 2 * (size_t)SP_PB * SP_T * SP_T + 2 * SP_PB * 4) *
+               sizeof(double2) + (2 * SP_T + SP_T * (SP_T + 1)) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
+    extern __shared__ double2 dsm[];
+    double2* UBs = dsm;                                  // [2][SP_UBN] boundary values [pp][b][part]
+    double2* Us = UBs + 2 * SP_UBN;                      // [SP_PB][2][4][SP_T]  V^-1 u_side
+    double2* Ds = Us + SP_PB * 2 * 4 * SP_T;             // [2][SP_PB][256] Dinv rows
+    double2* dEs = Ds + 2 * SP_PB * SP_T * SP_T;         // [2][SP_PB][4]   d_mk
+    double* as = reinterpret_cast<double*>(dEs + 2 * SP_PB * 4);
+    double* vis = as + 2 * SP_T;                         // V^-1, padded stride
     const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
     const int nrhs = a.R2 / 2;
     const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
     const int grp = blockIdx.y;
     int m0, m1;
     sp_group_range(a, grp, m0, m1);
-    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
     if (t < 2 * SP_T) as[t] = a.A01[t];
+    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
     const bool act = t < q2;
     const int ip = t % q, jp = t / q;
-    double g[2][3], Eacc[2][3];
+    double Eacc[2][3];
 #pragma unroll
     for (int part = 0; part < 2; ++part)
 #pragma unroll
         for (int kk = 0; kk < 3; ++kk) Eacc[part][kk] = 0.0;
     const size_t NIs = (size_t)a.nelem * q2;
     double* Eout = a.Ehat + (size_t)grp * a.nE * a.R2 * NIs + (size_t)leaf * q2 + t;
-    if (act) {
-        sp_load_g(a, leaf, k, t, g);
-        if (a.accumulate) {
+    if (act && a.accumulate) {
 #pragma unroll
-            for (int part = 0; part < 2; ++part)
+        for (int part = 0; part < 2; ++part)
 #pragma unroll
-                for (int kk = 0; kk < 3; ++kk)
-                    if (kk < a.nE) Eacc[part][kk] = Eout[((size_t)kk * a.R2 + 2 * k + part) * NIs];
-        }
+            for (int kk = 0; kk < 3; ++kk)
+                if (kk < a.nE) Eacc[part][kk] = Eout[((size_t)kk * a.R2 + 2 * k + part) * NIs];
     }
     const int* gb = a.gB + (size_t)leaf * nbnd;
     // edge pole sums: thread t < 2*nbnd owns (b, part) = (t/2, t%2) if the leaf owns node b
@@ -253,59 +274,72 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_down(SpecArgs a) {
                 if (kk < a.nE) Eg[kk] = Eeout[(size_t)kk * a.R2 * a.NE];
         }
     }
+    // prologue: batch 0 staged
     double2 pre[SP_UBR];
-    sp_fetch_ub(a, gb, k, m0, min(SP_PB, m1 - m0), nbnd, pre);
+    double2 pde = make_double2(0.0, 0.0);
+    const int de_pp = t >> 2, de_k = t & 3;              // d_mk staging task (t < 4 SP_PB)
+    {
+        const int nb0 = min(SP_PB, m1 - m0);
+        sp_fetch_ub(a, gb, k, m0, nb0, nbnd, pre);
+        sp_fetch_dinv(a, m0, nb0, Ds);
+        if (t < 4 * SP_PB && de_pp < nb0 && de_k < a.nE) pde = a.dE[(size_t)(m0 + de_pp) * a.nE + de_k];
 #pragma unroll
-    for (int u = 0; u < SP_UBR; ++u) UBs[0][t + u * SP_THREADS] = pre[u];
+        for (int u = 0; u < SP_UBR; ++u) UBs[t + u * SP_THREADS] = pre[u];
+        if (t < 4 * SP_PB) dEs[t] = pde;
+        cp_async_wait_all();
+    }
     __syncthreads();
-    const double c2 = a.c2;
+    const double mc2 = -a.c2;
+    // u^ task (fixed per thread): pp, part, side, r
     int buf = 0;
     for (int mb = m0; mb < m1; mb += SP_PB, buf ^= 1) {
         const int nbat = min(SP_PB, m1 - mb);
-        // next batch's boundary values in flight while this batch computes
-        if (mb + SP_PB < m1) sp_fetch_ub(a, gb, k, mb + SP_PB, min(SP_PB, m1 - mb - SP_PB), nbnd, pre);
-        const double2* ub = UBs[buf];
+        const bool more = mb + SP_PB < m1;
+        if (more) {
+            const int nbn = min(SP_PB, m1 - mb - SP_PB);
+            sp_fetch_ub(a, gb, k, mb + SP_PB, nbn, nbnd, pre);
+            sp_fetch_dinv(a, mb + SP_PB, nbn, Ds + (buf ^ 1) * SP_PB * SP_T * SP_T);
+            pde = make_double2(0.0, 0.0);
+            if (t < 4 * SP_PB && de_pp < nbn && de_k < a.nE) pde = a.dE[(size_t)(mb + SP_PB + de_pp) * a.nE + de_k];
+        }
+        const double2* ub = UBs + buf * SP_UBN;
         // u^_side = V^-1 u_side  (boundary order: bottom (i), right (j), top (i), left (j))
         for (int task = t; task < nbat * 128; task += blockDim.x) {
             const int pp = task >> 7, part = (task >> 6) & 1, side = (task >> 4) & 3, r = task & 15;
             if (r >= q) continue;
             const double2* u = ub + pp * 2 * nbnd + 2 * side * q + part;
+            const double* vr = vis + r * (SP_T + 1);
             double sx = 0.0, sy = 0.0;
             for (int j = 0; j < q; ++j) {
                 const double2 uv = u[2 * j];
-                const double v = vis[r * (SP_T + 1) + j];
+                const double v = vr[j];
                 sx = fma(v, uv.x, sx);
                 sy = fma(v, uv.y, sy);
             }
-            Us[pp][part][side][r] = make_double2(sx, sy);
+            Us[((pp * 2 + part) * 4 + side) * SP_T + r] = make_double2(sx, sy);
         }
         __syncthreads();
+        const double2* Db = Ds + buf * SP_PB * SP_T * SP_T;
+        const double2* dEb = dEs + buf * SP_PB * 4;
         if (act) {
             const double a0i = as[ip], a1i = as[SP_T + ip], a0j = as[jp], a1j = as[SP_T + jp];
 #pragma unroll
             for (int pp = 0; pp < SP_PB; ++pp) {
                 if (pp < nbat) {
-                    const int m = mb + pp;
-                    const double2* cf = a.cF + (size_t)m * a.nF;
-                    const double2 c0 = cf[0];
-                    const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0.0, 0.0);
-                    const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0.0, 0.0);
-                    const double2 d = __ldg(a.Dinv + (size_t)m * SP_T * SP_T + ip * SP_T + jp);
-                    const double2* de = a.dE + (size_t)m * a.nE;
-                    const double2 d0 = de[0], d1 = de[1];
-                    const double2 d2 = a.nE > 2 ? de[2] : make_double2(0.0, 0.0);
+                    const double2 d = Db[pp * SP_T * SP_T + ip * SP_T + jp];
+                    const double2 d0 = dEb[pp * 4 + 0], d1 = dEb[pp * 4 + 1], d2 = dEb[pp * 4 + 2];
 #pragma unroll
                     for (int part = 0; part < 2; ++part) {
-                        const double2 ubv = Us[pp][part][0][ip], ur = Us[pp][part][1][jp];
-                        const double2 ut = Us[pp][part][2][ip], ul = Us[pp][part][3][jp];
+                        const double2* U = Us + (pp * 2 + part) * 4 * SP_T;
+                        const double2 ubv = U[0 * SP_T + ip], ur = U[1 * SP_T + jp];
+                        const double2 ut = U[2 * SP_T + ip], ul = U[3 * SP_T + jp];
                         const double bx = a0i * ul.x + a1i * ur.x + ubv.x * a0j + ut.x * a1j;
                         const double by = a0i * ul.y + a1i * ur.y + ubv.y * a0j + ut.y * a1j;
-                        const double sx = c0.x * g[part][0] + c1v.x * g[part][1] + c2v.x * g[part][2] - c2 * bx;
-                        const double sy = c0.y * g[part][0] + c1v.y * g[part][1] + c2v.y * g[part][2] - c2 * by;
-                        const double wx = sx * d.x - sy * d.y, wy = sx * d.y + sy * d.x;
-                        Eacc[part][0] += d0.x * wx - d0.y * wy;
-                        Eacc[part][1] += d1.x * wx - d1.y * wy;
-                        Eacc[part][2] += d2.x * wx - d2.y * wy;
+                        // t = -c2 Dinv b
+                        const double tx = mc2 * (bx * d.x - by * d.y), ty = mc2 * (bx * d.y + by * d.x);
+                        Eacc[part][0] += d0.x * tx - d0.y * ty;
+                        Eacc[part][1] += d1.x * tx - d1.y * ty;
+                        Eacc[part][2] += d2.x * tx - d2.y * ty;
                     }
                 }
             }
@@ -313,17 +347,20 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_down(SpecArgs a) {
         if (eact) {
             for (int pp = 0; pp < nbat; ++pp) {
                 const double2 u = ub[pp * 2 * nbnd + t];
-                const double2* de = a.dE + (size_t)(mb + pp) * a.nE;
 #pragma unroll
-                for (int kk = 0; kk < 3; ++kk)
-                    if (kk < a.nE) Eg[kk] += de[kk].x * u.x - de[kk].y * u.y;
+                for (int kk = 0; kk < 3; ++kk) {
+                    const double2 de = dEb[pp * 4 + kk];
+                    Eg[kk] += de.x * u.x - de.y * u.y;
+                }
             }
         }
         // stage the prefetched batch; Us and UBs[buf] are rewritten after the barrier
-        if (mb + SP_PB < m1) {
+        if (more) {
 #pragma unroll
-            for (int u = 0; u < SP_UBR; ++u) UBs[buf ^ 1][t + u * SP_THREADS] = pre[u];
+            for (int u = 0; u < SP_UBR; ++u) UBs[(buf ^ 1) * SP_UBN + t + u * SP_THREADS] = pre[u];
+            if (t < 4 * SP_PB) dEs[(buf ^ 1) * SP_PB * 4 + t] = pde;
         }
+        cp_async_wait_all();
         __syncthreads();
     }
     if (act) {
@@ -341,8 +378,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_down(SpecArgs a) {
 }
 
 // --------------------------------------------------------------------------
-// k_spec_back: interior E_k = V (sum_groups E^_k) V^T and the owned edge nodes'
-// sums over groups   (grid: nelem * R2 CTAs)
+// k_spec_back: interior E_k = V (sum_groups E^_k + sum_f Pi_kf .* G_f) V^T and the
+// owned edge nodes' sums over groups   (grid: nelem * R2 CTAs)
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
     __shared__ double es[3][SP_T * SP_T];
@@ -353,10 +390,13 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
     const size_t NIs = (size_t)a.nelem * q2;
     for (int e = t; e < SP_T * SP_T; e += blockDim.x) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
     for (int e = t; e < a.nE * q2; e += blockDim.x) {
-        const int kk = e / q2, mode = e % q2;
+        const int kk = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
         const double* src = a.Ehat + ((size_t)kk * a.R2 + r2) * NIs + (size_t)leaf * q2 + mode;
         double s = 0.0;
         for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.R2 * NIs];
+        // pole-independent RHS part: sum_f Pi_kf G_f
+        const double* G = a.G + ((size_t)leaf * a.R2 + r2) * a.nF * q2 + mode;
+        for (int f = 0; f < a.nF; ++f) s += a.Pi[((size_t)kk * a.nF + f) * SP_T * SP_T + ip * SP_T + jp] * G[(size_t)f * q2];
         es[kk][mode] = s;   // E^[i'][j'] at j'*q + i'
     }
     for (int e = t; e < a.nE * nbnd; e += blockDim.x) {

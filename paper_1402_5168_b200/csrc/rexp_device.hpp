@@ -79,7 +79,7 @@ class DeviceStore {
     int *d_elem_g = nullptr, *d_leaf_gB = nullptr, *d_rpos1 = nullptr, *d_rpos2 = nullptr, *d_rgs = nullptr;
     double2 *d_cF = nullptr, *d_dE = nullptr, *d_Dinv = nullptr;
     double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_E01 = nullptr, *d_A01 = nullptr;
-    double *d_G = nullptr, *d_Ehat = nullptr, *d_Eedge = nullptr;   // spectral RHS fields, pole-sum partials
+    double *d_G = nullptr, *d_Ehat = nullptr, *d_Eedge = nullptr, *d_Pi = nullptr;   // spectral RHS fields, pole-sum partials
     int* d_leaf_own = nullptr;                  // [nelem][4q] edge-node ownership for the pole sums
     int ngroups = 1;                            // pole groups per leaf CTA (spectral path)
     int chunk = 1;             // half poles per work-buffer chunk
