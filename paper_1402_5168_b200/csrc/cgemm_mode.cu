@@ -9,32 +9,38 @@ namespace rexp {
 namespace dev {
 namespace {
 
-template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1>
+template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int MINB = 1>
 void cg_launch(dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    k_cgemm<MT, WN, BK, R2T, MODE, 1, 1, WM><<<grid, 32 * WN * WM, cgemm_smem_bytes<MT, WN, BK, 1, WM>(), s>>>(a);
+    k_cgemm<MT, WN, BK, R2T, MODE, 1, MINB, WM><<<grid, 32 * WN * WM, cgemm_smem_bytes<MT, WN, BK, 1, WM>(), s>>>(a);
 }
 // leaf tiles: MT in {4, 5}, WN = 8; merge tiles: MT in {2, 4} with
 //   WN = 8, WM = 1 | WN = 4, WM = 2 | WN = 2, WM = 4
+template <int BK, int R2T, int MODE, int MINB>
+void cg_tiles_b(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    if (MT == 2) {
+        if (WN == 2) cg_launch<2, 2, BK, R2T, MODE, 4, MINB>(grid, s, a);
+        else if (WN == 4) cg_launch<2, 4, BK, R2T, MODE, 2, MINB>(grid, s, a);
+        else cg_launch<2, 8, BK, R2T, MODE, 1, MINB>(grid, s, a);
+    } else {
+        if (WN == 2) cg_launch<4, 2, BK, R2T, MODE, 4, MINB>(grid, s, a);
+        else if (WN == 4) cg_launch<4, 4, BK, R2T, MODE, 2, MINB>(grid, s, a);
+        else cg_launch<4, 8, BK, R2T, MODE, 1, MINB>(grid, s, a);
+    }
+}
+// MINB = 4: register budget for 4 resident 256-thread CTAs per SM (<= 64 registers)
 template <int BK, int R2T, int MODE>
-void cg_tiles(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+void cg_tiles(int MT, int WN, int MINB, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     if (MODE == CG_LEAF_UP || MODE == CG_LEAF_DOWN) {
         if (MT == 4) cg_launch<4, 8, BK, R2T, MODE>(grid, s, a);
         else cg_launch<5, 8, BK, R2T, MODE>(grid, s, a);
         return;
     }
-    if (MT == 2) {
-        if (WN == 2) cg_launch<2, 2, BK, R2T, MODE, 4>(grid, s, a);
-        else if (WN == 4) cg_launch<2, 4, BK, R2T, MODE, 2>(grid, s, a);
-        else cg_launch<2, 8, BK, R2T, MODE>(grid, s, a);
-    } else {
-        if (WN == 2) cg_launch<4, 2, BK, R2T, MODE, 4>(grid, s, a);
-        else if (WN == 4) cg_launch<4, 4, BK, R2T, MODE, 2>(grid, s, a);
-        else cg_launch<4, 8, BK, R2T, MODE>(grid, s, a);
-    }
+    if (MINB >= 4) cg_tiles_b<BK, R2T, MODE, 4>(MT, WN, grid, s, a);
+    else cg_tiles_b<BK, R2T, MODE, 1>(MT, WN, grid, s, a);
 }
-template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1>
+template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int MINB = 1>
 void cg_allow1() {
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2T, MODE, 1, 1, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2T, MODE, 1, MINB, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
 }
 template <int BK, int R2T, int MODE>
@@ -45,22 +51,24 @@ void cg_allow_tiles() {
     }
     cg_allow1<2, 2, BK, R2T, MODE, 4>(); cg_allow1<2, 4, BK, R2T, MODE, 2>(); cg_allow1<2, 8, BK, R2T, MODE>();
     cg_allow1<4, 2, BK, R2T, MODE, 4>(); cg_allow1<4, 4, BK, R2T, MODE, 2>(); cg_allow1<4, 8, BK, R2T, MODE>();
+    cg_allow1<2, 2, BK, R2T, MODE, 4, 4>(); cg_allow1<2, 4, BK, R2T, MODE, 2, 4>(); cg_allow1<2, 8, BK, R2T, MODE, 1, 4>();
+    cg_allow1<4, 2, BK, R2T, MODE, 4, 4>(); cg_allow1<4, 4, BK, R2T, MODE, 2, 4>(); cg_allow1<4, 8, BK, R2T, MODE, 1, 4>();
 }
 
 // BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16;
 // R2 = 2, 4 compiled in, anything else at run time
-void run(int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+void run(int R2, int MT, int WN, int MINB, int K, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     constexpr int M = CG_MODE;
     const bool b28 = (K % 28) == 0;
     if (R2 == 2) {
-        if (b28) cg_tiles<28, 2, M>(MT, WN, grid, s, a);
-        else cg_tiles<16, 2, M>(MT, WN, grid, s, a);
+        if (b28) cg_tiles<28, 2, M>(MT, WN, MINB, grid, s, a);
+        else cg_tiles<16, 2, M>(MT, WN, MINB, grid, s, a);
     } else if (R2 == 4) {
-        if (b28) cg_tiles<28, 4, M>(MT, WN, grid, s, a);
-        else cg_tiles<16, 4, M>(MT, WN, grid, s, a);
+        if (b28) cg_tiles<28, 4, M>(MT, WN, MINB, grid, s, a);
+        else cg_tiles<16, 4, M>(MT, WN, MINB, grid, s, a);
     } else {
-        if (b28) cg_tiles<28, 0, M>(MT, WN, grid, s, a);
-        else cg_tiles<16, 0, M>(MT, WN, grid, s, a);
+        if (b28) cg_tiles<28, 0, M>(MT, WN, MINB, grid, s, a);
+        else cg_tiles<16, 0, M>(MT, WN, MINB, grid, s, a);
     }
 }
 void allow() {
@@ -73,22 +81,22 @@ void allow() {
 }  // namespace
 
 #if CG_MODE == 0
-void cg_run_leaf_up(int R2, int MT, int WN, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, K, g, s, a); }
+void cg_run_leaf_up(int R2, int MT, int WN, int MINB, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, MINB, K, g, s, a); }
 void cg_allow_leaf_up() { allow(); }
 #elif CG_MODE == 1
-void cg_run_leaf_down(int R2, int MT, int WN, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, K, g, s, a); }
+void cg_run_leaf_down(int R2, int MT, int WN, int MINB, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, MINB, K, g, s, a); }
 void cg_allow_leaf_down() { allow(); }
 #elif CG_MODE == 2
-void cg_run_upx(int R2, int MT, int WN, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, K, g, s, a); }
+void cg_run_upx(int R2, int MT, int WN, int MINB, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, MINB, K, g, s, a); }
 void cg_allow_upx() { allow(); }
 #elif CG_MODE == 3
-void cg_run_upy(int R2, int MT, int WN, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, K, g, s, a); }
+void cg_run_upy(int R2, int MT, int WN, int MINB, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, MINB, K, g, s, a); }
 void cg_allow_upy() { allow(); }
 #elif CG_MODE == 4
-void cg_run_down(int R2, int MT, int WN, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, K, g, s, a); }
+void cg_run_down(int R2, int MT, int WN, int MINB, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, MINB, K, g, s, a); }
 void cg_allow_down() { allow(); }
 #else
-void cg_run_root(int R2, int MT, int WN, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, K, g, s, a); }
+void cg_run_root(int R2, int MT, int WN, int MINB, int K, dim3 g, cudaStream_t s, const CgemmArgs& a) { run(R2, MT, WN, MINB, K, g, s, a); }
 void cg_allow_root() { allow(); }
 #endif
 

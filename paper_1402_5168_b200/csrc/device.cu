@@ -1206,7 +1206,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
             a.nrowblk = (ns + 8 * cfg.MT * cg_wm(cfg.WN) - 1) / (8 * cfg.MT * cg_wm(cfg.WN));
             const int ncb = (R2 + 8 * cfg.WN - 1) / (8 * cfg.WN);
             tbeg(s);
-            cg_run_mode(CG_ROOT, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
+            cg_run_mode(CG_ROOT, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, a, cfg.minb);
             tend(T_ROOT, s);
         } else {
             GemvArgs g = gemv_shape(ns, ns, 1, true);
@@ -1248,7 +1248,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
         a.nrowblk = (a.rows + bm - 1) / bm;
         const int ncb = (L.nodes * R2 + 8 * cfg.WN - 1) / (8 * cfg.WN);
         tbeg(s);
-        cg_run_mode(mode, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, a);
+        cg_run_mode(mode, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, a, cfg.minb);
         tend(cls, s);
         return REXP_OK;
     }
@@ -1338,12 +1338,13 @@ int DeviceStore::tune_stages(bool measure) {
     };
     auto tune = [&](int kind, size_t li, StageCfg& best) {
         std::vector<StageCfg> cands;
-        for (int mt : {2, 4})
-            for (int wn : {2, 4, 8}) {
-                StageCfg c;
-                c.kind = 0; c.MT = mt; c.WN = wn;
-                cands.push_back(c);
-            }
+        for (int minb : {1, 4})
+            for (int mt : {2, 4})
+                for (int wn : {2, 4, 8}) {
+                    StageCfg c;
+                    c.kind = 0; c.MT = mt; c.WN = wn; c.minb = minb;
+                    cands.push_back(c);
+                }
         if (gemv_ok) {
             StageCfg c;
             c.kind = 1;
@@ -1372,7 +1373,8 @@ int DeviceStore::tune_stages(bool measure) {
 std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
         return c.kind == 1 ? std::string("gemv")
-                           : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN);
+                           : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
+                                 (c.minb > 1 ? "r" : "");
     };
     std::string s = tuned ? "tuned:" : "default:";
     for (size_t li = 0; li < levels.size(); ++li)

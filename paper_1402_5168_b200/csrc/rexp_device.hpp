@@ -14,6 +14,7 @@ namespace dev {
 struct StageCfg {
     int kind = 0;   // 0: DMMA GEMM (k_cgemm), 1: GEMV (k_gemv)
     int MT = 4, WN = 8;
+    int minb = 1;   // 4: register-capped variant (4 resident CTAs per SM)
 };
 
 struct Level {
