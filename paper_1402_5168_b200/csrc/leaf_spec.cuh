@@ -18,8 +18,11 @@
 //   UP:   h = N_I V W V^T (outward flux) from W through e_s = V^T d_s (four q-vectors).
 //   DOWN: E^_k += Re(d_mk W_m), the interior solutions u_m are never formed.
 // One CTA owns one (leaf, right-hand side) with both real parts and a
-// contiguous group of half poles; thread t < q^2 owns spectral mode
-// t = j' q + i'.
+// contiguous group of half poles; thread t owns spectral mode (i', j') =
+// (t & 15, t >> 4) of the zero-padded 16 x 16 grid (active when i', j' < q;
+// compact mode index j' q + i' in G and E^).  Dinv is symmetric in (i', j'),
+// so the thread reads it at t = j' 16 + i': consecutive threads, consecutive
+// addresses (global and shared).
 #pragma once
 
 namespace rexp {
@@ -112,7 +115,7 @@ __device__ __forceinline__ void sp_load_g(const SpecArgs& a, int leaf, int k, in
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
     __shared__ double2 Ws[SP_PB][2][SP_T * SP_LW];  // W[i'][j'] at j'*SP_LW + i'
-    __shared__ double2 Ys[SP_PB][2][4][SP_T];       // y0, y1, z0, z1
+    __shared__ double2 Ys[SP_PB][2][4 * SP_T + 1];  // y0, y1, z0, z1 (+1: parts on different banks)
     __shared__ double vs[SP_T * (SP_T + 1)];
     __shared__ double es[2 * SP_T];
     const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
@@ -122,11 +125,11 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
     sp_group_range(a, blockIdx.y, m0, m1);
     for (int e = t; e < SP_T * SP_T; e += blockDim.x) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
     if (t < 2 * SP_T) es[t] = a.E01[t];
-    const bool act = t < q2;
-    const int ip = t % q, jp = t / q;
+    const int ip = t & 15, jp = t >> 4;
+    const bool act = ip < q && jp < q;
     const int wpos = jp * SP_LW + ip;
     double g[2][3];
-    if (act) sp_load_g(a, leaf, k, t, g);
+    if (act) sp_load_g(a, leaf, k, jp * q + ip, g);
     __syncthreads();
     for (int mb = m0; mb < m1; mb += SP_PB) {
         const int nbat = min(SP_PB, m1 - mb);
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
                     const double2 c0 = cf[0];
                     const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0.0, 0.0);
                     const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0.0, 0.0);
-                    const double2 d = __ldg(a.Dinv + (size_t)m * SP_T * SP_T + ip * SP_T + jp);
+                    const double2 d = __ldg(a.Dinv + (size_t)m * SP_T * SP_T + t);
 #pragma unroll
                     for (int part = 0; part < 2; ++part) {
                         const double sx = c0.x * g[part][0] + c1v.x * g[part][1] + c2v.x * g[part][2];
@@ -165,8 +168,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
                 s0x = fma(w.x, e0, s0x); s0y = fma(w.y, e0, s0y);
                 s1x = fma(w.x, e1, s1x); s1y = fma(w.y, e1, s1y);
             }
-            Ys[pp][part][2 * col][r] = make_double2(s0x, s0y);
-            Ys[pp][part][2 * col + 1][r] = make_double2(s1x, s1y);
+            Ys[pp][part][(2 * col) * SP_T + r] = make_double2(s0x, s0y);
+            Ys[pp][part][(2 * col + 1) * SP_T + r] = make_double2(s1x, s1y);
         }
         __syncthreads();
         // bottom: -c1 V y0, right: +c1 V z1, top: +c1 V y1, left: -c1 V z0
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
             const int side = b / q, s1 = b % q;
             const int vec = side == 0 ? 0 : side == 1 ? 3 : side == 2 ? 1 : 2;
             const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
-            const double2* y = Ys[pp][part][vec];
+            const double2* y = Ys[pp][part] + vec * SP_T;
             double sx = 0.0, sy = 0.0;
             for (int kk = 0; kk < q; ++kk) {
                 const double v = vs[s1 * (SP_T + 1) + kk];
@@ -245,15 +248,15 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
     sp_group_range(a, grp, m0, m1);
     if (t < 2 * SP_T) as[t] = a.A01[t];
     for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
-    const bool act = t < q2;
-    const int ip = t % q, jp = t / q;
+    const int ip = t & 15, jp = t >> 4;
+    const bool act = ip < q && jp < q;
     double Eacc[2][3];
 #pragma unroll
     for (int part = 0; part < 2; ++part)
 #pragma unroll
         for (int kk = 0; kk < 3; ++kk) Eacc[part][kk] = 0.0;
     const size_t NIs = (size_t)a.nelem * q2;
-    double* Eout = a.Ehat + (size_t)grp * a.nE * a.R2 * NIs + (size_t)leaf * q2 + t;
+    double* Eout = a.Ehat + (size_t)grp * a.nE * a.R2 * NIs + (size_t)leaf * q2 + (jp * q + ip);
     if (act && a.accumulate) {
 #pragma unroll
         for (int part = 0; part < 2; ++part)
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
 #pragma unroll
             for (int pp = 0; pp < SP_PB; ++pp) {
                 if (pp < nbat) {
-                    const double2 d = Db[pp * SP_T * SP_T + ip * SP_T + jp];
+                    const double2 d = Db[pp * SP_T * SP_T + t];
                     const double2 d0 = dEb[pp * 4 + 0], d1 = dEb[pp * 4 + 1], d2 = dEb[pp * 4 + 2];
 #pragma unroll
                     for (int part = 0; part < 2; ++part) {
