@@ -121,18 +121,18 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
     """Algorithmic FP64 flops and operator bytes per step, per kernel class.
     Complex multiply-add = 8 flops, complex x real multiply-add = 4, complex
     product = 6; operator element = 16 bytes.  leaf = "spectral" counts the
-    per-pole work of the spectral leaf kernels, per (half pole, leaf, real part):
-      UP:   W = Dinv .* sum_f c_f G_f   q^2 (4 nF + 6)
-            y_s, z_s (4 weighted row/column sums)            16 q^2
-            h = +-c1 V y (4 sides)                            16 q^2
-      DOWN: u^ = V^-1 u_side (4 sides)                        16 q^2
-            boundary outer products b (4 complex x real)      16 q^2
+    per-pole work of the spectral leaf kernels, per (half pole, leaf, real part);
+    edge data live in the spectral edge basis, so neither kernel
+    multiplies by V or V^-1 per pole:
+      UP:   W = Dinv .* sum_f c_f G_f                          q^2 (4 nF + 6)
+            y_s, z_s (4 weighted row/column sums) = the flux   16 q^2
+      DOWN: boundary outer products b (4 complex x real)      16 q^2
             t = -c2 Dinv b, pole sums Re(d_k t)               q^2 (8 + 4 nE)
-            owned edge nodes' pole sums                       2q * 4 nE
-            (the RHS-field part of the pole sum is pole-independent,
-            sum_m Re(d_mk c_mf Dinv_m) =: Pi_kf, applied once per step in k_spec_back)
-    The once-per-step transforms (k_spec_pre, k_spec_back) are O(q^3) per leaf,
-    not per pole, and are counted under pre / pole_sum."""
+            owned edge segments' pole sums                    2q * 4 nE
+    (the RHS-field part of the pole sum is pole-independent, sum_m Re(d_mk c_mf
+    Dinv_m) =: Pi_kf, applied once per step in k_spec_back).  The once-per-step
+    transforms (k_spec_pre, k_spec_back) are O(q^3) per leaf, not per pole.
+    """
     n, q = cfg["n"], cfg["p"] - 2
     q2, e = q * q, n * n
     lv = tree_dims(n, q)
@@ -140,15 +140,18 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
     merge = {
         "merge_up": (sum(nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx in lv),
                      sum(nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx in lv)),
-        "root": (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16),
+        # shared store: Fourier root (two DFTs over the n elements of the 2nq seam
+        # unknowns, n blocks of (2q)^2); per-node: dense (2nq)^2
+        "root": ((nh * R2 * (2 * 2 * n * q * n * 8 + n * (2 * q) ** 2 * 8), nh * n * (2 * q) ** 2 * 16) if shared
+                 else (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16)),
         "merge_down": (sum(nh * nd * n3 * nx * R2 * 8 for nd, n3, nx in lv),
                        sum(nh * per(nd) * n3 * nx * 16 for nd, n3, nx in lv)),
     }
     if leaf == "spectral":
         unit = nh * e * R2
         w = {
-            "leaf_up": (unit * q2 * (4 * nF + 6 + 32), nh * q2 * 16),
-            "leaf_down": (unit * (32 * q2 + q2 * (8 + 4 * nE) + 8 * q * nE), nh * q2 * 16),
+            "leaf_up": (unit * q2 * (4 * nF + 6 + 16), nh * q2 * 16),
+            "leaf_down": (unit * (16 * q2 + q2 * (8 + 4 * nE) + 8 * q * nE), nh * q2 * 16),
         }
         w.update(merge)
         return w

@@ -150,7 +150,9 @@ int rexp_setup(const rexp_problem* prob, double tau, double delta, double Lambda
         for (int c0 = h->h0; c0 < h->h1; c0 += static_cast<int>(cmax)) {
             const int c1 = static_cast<int>(std::min<int64_t>(h->h1, c0 + cmax));
             std::vector<HostLevelOps> ops;
-            if ((rc = factor_host(h->P, h->T, h->pt, c0, c1, h->shared, opt.nthreads, ops, h->shared))) return rc;
+            if ((rc = factor_host(h->P, h->T, h->pt, c0, c1, h->shared, opt.nthreads, ops, h->shared,
+                                  h->dev->fdm)))
+                return rc;
             if ((rc = h->dev->upload_ops(ops, c0 - h->h0))) return rc;
         }
         if ((rc = h->dev->tune_stages(true))) return rc;

@@ -1112,16 +1112,17 @@ void allow_all() {
     allow_all_nb<R2, 8>();
 }
 
-GemvArgs gemv_shape(int rows, int cols, int nodes, bool shared) {
+GemvArgs gemv_shape(int rows, int cols, int nodes, bool shared, int rbmax = 64) {
     GemvArgs g{};
     g.rows = rows;
     g.cols = cols;
     g.nodes = nodes;
     g.shared = shared ? 1 : 0;
-    // 64-row blocks split 4 ways over columns: many CTAs and >= 8 loads in
-    // flight per thread keep the HBM stream of the top (1-2 node) levels busy
+    // rbmax-row blocks (default 64) split 256/rb ways over columns: many CTAs and
+    // >= 8 loads in flight per thread keep the HBM stream of the top levels busy;
+    // the autotuner also tries 32/128/256-row blocks (CTA count vs wave tail)
     int rb = ((rows + 31) / 32) * 32;
-    if (rb > 64) rb = 64;
+    if (rb > rbmax) rb = rbmax;
     g.RB = rb;
     g.CS = 256 / rb;
     if (g.CS > 8) g.CS = 8;
@@ -1209,7 +1210,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
             cg_run_mode(CG_ROOT, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, a, cfg.minb);
             tend(T_ROOT, s);
         } else {
-            GemvArgs g = gemv_shape(ns, ns, 1, true);
+            GemvArgs g = gemv_shape(ns, ns, 1, true, cfg.rb);
             g.shared = 1;
             g.M = Xr; g.xsrc = hr; g.xsrc_ps = hstride; g.xi0 = d_rpos1; g.xi1 = d_rpos2;
             g.ydst = d_edge; g.ydst_ps = NE; g.yo = d_rgs;
@@ -1255,16 +1256,16 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     const int NB = pick_nb(L.nodes, R2, shared);
     GemvArgs g;
     if (kind == 0) {
-        g = gemv_shape(L.n3, L.n3, L.nodes, shared);
+        g = gemv_shape(L.n3, L.n3, L.nodes, shared, cfg.rb);
         g.M = L.X + static_cast<size_t>(m0) * L.ppX; g.xsrc = hc; g.xsrc_ps = hstride; g.xi0 = L.ia3; g.xi1 = L.ib3;
         g.ydst = L.w3; g.ydst_ps = static_cast<long long>(L.nodes) * L.n3;
     } else if (kind == 1) {
-        g = gemv_shape(L.next, L.n3, L.nodes, shared);
+        g = gemv_shape(L.next, L.n3, L.nodes, shared, cfg.rb);
         g.M = L.Y + static_cast<size_t>(m0) * L.ppY; g.xsrc = L.w3; g.xsrc_ps = static_cast<long long>(L.nodes) * L.n3;
         g.ysrc = hc; g.ysrc_ps = hstride; g.yi = L.ext;
         g.ydst = hp; g.ydst_ps = hstride;
     } else {
-        g = gemv_shape(L.n3, L.next, L.nodes, shared);
+        g = gemv_shape(L.n3, L.next, L.nodes, shared, cfg.rb);
         g.M = L.S + static_cast<size_t>(m0) * L.ppS; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
         g.ysrc = L.w3; g.ysrc_ps = static_cast<long long>(L.nodes) * L.n3;
         g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
@@ -1346,9 +1347,11 @@ int DeviceStore::tune_stages(bool measure) {
                     cands.push_back(c);
                 }
         if (gemv_ok) {
-            StageCfg c;
-            c.kind = 1;
-            cands.push_back(c);
+            for (int rb : {32, 64, 128, 256}) {
+                StageCfg c;
+                c.kind = 1; c.rb = rb;
+                cands.push_back(c);
+            }
         }
         float bt = time_cfg(kind, li, best);
         for (const StageCfg& c : cands) {
@@ -1372,7 +1375,7 @@ int DeviceStore::tune_stages(bool measure) {
 
 std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
-        return c.kind == 1 ? std::string("gemv")
+        return c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
                                  (c.minb > 1 ? "r" : "");
     };

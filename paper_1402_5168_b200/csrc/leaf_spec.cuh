@@ -111,19 +111,20 @@ __device__ __forceinline__ void sp_load_g(const SpecArgs& a, int leaf, int k, in
 }
 
 // --------------------------------------------------------------------------
-// k_leaf_spec_up: h_m = N_I A_m^-1 f_m   (grid: nelem * nrhs, ngroups)
+// k_leaf_spec_up: h_m = N_I A_m^-1 f_m in the edge basis   (grid: nelem * nrhs, ngroups)
+// Per batch of SP_PB half poles: thread (i', j') forms W = Dinv_m .* sum_f c_mf G_f;
+// then task (pp, part, row|col, r) forms y_s[r] = sum_j' W[r][j'] e_s[j'] (rows) or
+// z_s[r] = sum_i' W[i'][r] e_s[i'] (columns), s = 0, 1, and writes the flux
+//   bottom -c1 y0, top +c1 y1, left -c1 z0, right +c1 z1   (edge basis: no V).
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
     __shared__ double2 Ws[SP_PB][2][SP_T * SP_LW];  // W[i'][j'] at j'*SP_LW + i'
-    __shared__ double2 Ys[SP_PB][2][4 * SP_T + 1];  // y0, y1, z0, z1 (+1: parts on different banks)
-    __shared__ double vs[SP_T * (SP_T + 1)];
     __shared__ double es[2 * SP_T];
-    const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
+    const int q = a.q, nbnd = 4 * q, t = threadIdx.x;
     const int nrhs = a.R2 / 2;
     const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
     int m0, m1;
     sp_group_range(a, blockIdx.y, m0, m1);
-    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
     if (t < 2 * SP_T) es[t] = a.E01[t];
     const int ip = t & 15, jp = t >> 4;
     const bool act = ip < q && jp < q;
@@ -154,8 +155,6 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
             }
         }
         __syncthreads();
-        // rows:    y_s[i'] = sum_j' W[i'][j'] e_s[j']   (s = 0, 1 in one pass)
-        // columns: z_s[j'] = sum_i' W[i'][j'] e_s[i']
         for (int task = t; task < nbat * 64; task += blockDim.x) {
             const int pp = task >> 6, part = (task >> 5) & 1, col = (task >> 4) & 1, r = task & 15;
             if (r >= q) continue;
@@ -168,28 +167,12 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
                 s0x = fma(w.x, e0, s0x); s0y = fma(w.y, e0, s0y);
                 s1x = fma(w.x, e1, s1x); s1y = fma(w.y, e1, s1y);
             }
-            Ys[pp][part][(2 * col) * SP_T + r] = make_double2(s0x, s0y);
-            Ys[pp][part][(2 * col + 1) * SP_T + r] = make_double2(s1x, s1y);
+            double2* hb = a.h + ((size_t)(mb + pp) * a.hps + (size_t)leaf * nbnd) * a.R2 + 2 * k + part;
+            const int side0 = col ? 3 : 0, side1 = col ? 1 : 2;   // (bottom, top) or (left, right)
+            hb[(size_t)(side0 * q + r) * a.R2] = make_double2(-a.c1 * s0x, -a.c1 * s0y);
+            hb[(size_t)(side1 * q + r) * a.R2] = make_double2(a.c1 * s1x, a.c1 * s1y);
         }
-        __syncthreads();
-        // bottom: -c1 V y0, right: +c1 V z1, top: +c1 V y1, left: -c1 V z0
-        for (int task = t; task < nbat * nbnd * 2; task += blockDim.x) {
-            const int pp = task / (2 * nbnd), rem = task % (2 * nbnd), b = rem >> 1, part = rem & 1;
-            const int side = b / q, s1 = b % q;
-            const int vec = side == 0 ? 0 : side == 1 ? 3 : side == 2 ? 1 : 2;
-            const double sgn = (side == 0 || side == 3) ? -a.c1 : a.c1;
-            const double2* y = Ys[pp][part] + vec * SP_T;
-            double sx = 0.0, sy = 0.0;
-            for (int kk = 0; kk < q; ++kk) {
-                const double v = vs[s1 * (SP_T + 1) + kk];
-                sx = fma(v, y[kk].x, sx);
-                sy = fma(v, y[kk].y, sy);
-            }
-            a.h[((size_t)(mb + pp) * a.hps + (size_t)leaf * nbnd + b) * a.R2 + 2 * k + part] =
-                make_double2(sgn * sx, sgn * sy);
-        }
-        // the next batch writes Ws (last read before the barrier above) and Ys
-        // (read here; its next writer runs after the next batch's first barrier)
+        __syncthreads();   // Ws is rewritten by the next batch
     }
 }
 
@@ -200,7 +183,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
 //   sum_m Re(d_mk c_mf Dinv_m) =: Pi_kf   (setup, device.cu),
 // and is added once per step in k_spec_back; per pole only
 //   E^_k += Re((-c2 d_mk) Dinv_m .* b_m),  b_m = a0^ ul^T + a1^ ur^T + ub^ a0^T + ut^ a1^T
-// remains, plus the pole sums of the edge nodes this leaf owns.
+// remains (u^_side: the edge values, already in the edge basis), plus the
+// (edge-basis) pole sums of the edge segments this leaf owns.
 // Per batch of SP_PB half poles the boundary values (registers) and the Dinv
 // rows (cp.async) of the NEXT batch are in flight while this batch computes.
 //   (grid: nelem * nrhs, ngroups; dynamic shared memory sp_down_smem())
@@ -208,15 +192,24 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
 constexpr int SP_UBN = SP_PB * 2 * SP_NB;              // boundary values staged per batch
 constexpr int SP_UBR = (SP_UBN + SP_THREADS - 1) / SP_THREADS;
 
+// staged layout [pp][part][b]: consecutive modes read consecutive banks
 __device__ __forceinline__ void sp_fetch_ub(const SpecArgs& a, const int* gb, int k, int mb, int nbat, int nbnd,
                                             double2 (&r)[SP_UBR]) {
 #pragma unroll
     for (int u = 0; u < SP_UBR; ++u) {
-        const int task = threadIdx.x + u * SP_THREADS;   // (pp, b, part), part fastest
+        const int task = threadIdx.x + u * SP_THREADS;   // (pp, b, part), part fastest: coalesced reads
         const int pp = task / (2 * nbnd), rem = task % (2 * nbnd);
         r[u] = make_double2(0.0, 0.0);
         if (pp < nbat)
             r[u] = a.edge[((size_t)(mb + pp) * a.NE + gb[rem >> 1]) * a.R2 + 2 * k + (rem & 1)];
+    }
+}
+__device__ __forceinline__ void sp_stage_ub(const double2 (&r)[SP_UBR], int nbnd, double2* dst) {
+#pragma unroll
+    for (int u = 0; u < SP_UBR; ++u) {
+        const int task = threadIdx.x + u * SP_THREADS;
+        const int pp = task / (2 * nbnd), rem = task % (2 * nbnd);
+        if (pp < SP_PB) dst[(pp * 2 + (rem & 1)) * SP_NB + (rem >> 1)] = r[u];
     }
 }
 
@@ -228,18 +221,16 @@ __device__ __forceinline__ void sp_fetch_dinv(const SpecArgs& a, int mb, int nba
 }
 
 constexpr size_t sp_down_smem() {
-    return (2 * (size_t)SP_UBN + (size_t)SP_PB * 2 * 4 * SP_T + 2 * (size_t)SP_PB * SP_T * SP_T + 2 * SP_PB * 4) *
-               sizeof(double2) + (2 * SP_T + SP_T * (SP_T + 1)) * sizeof(double);
+    return (2 * (size_t)SP_UBN + 2 * (size_t)SP_PB * SP_T * SP_T + 2 * SP_PB * 4) * sizeof(double2) +
+           2 * SP_T * sizeof(double);
 }
 
 __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
     extern __shared__ double2 dsm[];
-    double2* UBs = dsm;                                  // [2][SP_UBN] boundary values [pp][b][part]
-    double2* Us = UBs + 2 * SP_UBN;                      // [SP_PB][2][4][SP_T]  V^-1 u_side
-    double2* Ds = Us + SP_PB * 2 * 4 * SP_T;             // [2][SP_PB][256] Dinv rows
+    double2* UBs = dsm;                                  // [2][SP_PB][2][SP_NB] edge-basis boundary values
+    double2* Ds = UBs + 2 * SP_UBN;                      // [2][SP_PB][256] Dinv rows
     double2* dEs = Ds + 2 * SP_PB * SP_T * SP_T;         // [2][SP_PB][4]   d_mk
     double* as = reinterpret_cast<double*>(dEs + 2 * SP_PB * 4);
-    double* vis = as + 2 * SP_T;                         // V^-1, padded stride
     const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
     const int nrhs = a.R2 / 2;
     const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
@@ -247,7 +238,6 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
     int m0, m1;
     sp_group_range(a, grp, m0, m1);
     if (t < 2 * SP_T) as[t] = a.A01[t];
-    for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
     const int ip = t & 15, jp = t >> 4;
     const bool act = ip < q && jp < q;
     double Eacc[2][3];
@@ -265,12 +255,13 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
                 if (kk < a.nE) Eacc[part][kk] = Eout[((size_t)kk * a.R2 + 2 * k + part) * NIs];
     }
     const int* gb = a.gB + (size_t)leaf * nbnd;
-    // edge pole sums: thread t < 2*nbnd owns (b, part) = (t/2, t%2) if the leaf owns node b
-    const bool eact = t < 2 * nbnd && a.own[(size_t)leaf * nbnd + (t >> 1)];
+    // edge pole sums: thread t < 2*nbnd owns (b, part) = (t >> 1, t & 1) if the leaf owns node b
+    const int e_b = t >> 1, e_part = t & 1;
+    const bool eact = t < 2 * nbnd && a.own[(size_t)leaf * nbnd + e_b];
     double Eg[3] = {0.0, 0.0, 0.0};
     double* Eeout = nullptr;
     if (eact) {
-        Eeout = a.Eedge + (size_t)grp * a.nE * a.R2 * a.NE + (size_t)(2 * k + (t & 1)) * a.NE + gb[t >> 1];
+        Eeout = a.Eedge + (size_t)grp * a.nE * a.R2 * a.NE + (size_t)(2 * k + e_part) * a.NE + gb[e_b];
         if (a.accumulate) {
 #pragma unroll
             for (int kk = 0; kk < 3; ++kk)
@@ -286,14 +277,12 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
         sp_fetch_ub(a, gb, k, m0, nb0, nbnd, pre);
         sp_fetch_dinv(a, m0, nb0, Ds);
         if (t < 4 * SP_PB && de_pp < nb0 && de_k < a.nE) pde = a.dE[(size_t)(m0 + de_pp) * a.nE + de_k];
-#pragma unroll
-        for (int u = 0; u < SP_UBR; ++u) UBs[t + u * SP_THREADS] = pre[u];
+        sp_stage_ub(pre, nbnd, UBs);
         if (t < 4 * SP_PB) dEs[t] = pde;
         cp_async_wait_all();
     }
     __syncthreads();
     const double mc2 = -a.c2;
-    // u^ task (fixed per thread): pp, part, side, r
     int buf = 0;
     for (int mb = m0; mb < m1; mb += SP_PB, buf ^= 1) {
         const int nbat = min(SP_PB, m1 - mb);
@@ -306,22 +295,6 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
             if (t < 4 * SP_PB && de_pp < nbn && de_k < a.nE) pde = a.dE[(size_t)(mb + SP_PB + de_pp) * a.nE + de_k];
         }
         const double2* ub = UBs + buf * SP_UBN;
-        // u^_side = V^-1 u_side  (boundary order: bottom (i), right (j), top (i), left (j))
-        for (int task = t; task < nbat * 128; task += blockDim.x) {
-            const int pp = task >> 7, part = (task >> 6) & 1, side = (task >> 4) & 3, r = task & 15;
-            if (r >= q) continue;
-            const double2* u = ub + pp * 2 * nbnd + 2 * side * q + part;
-            const double* vr = vis + r * (SP_T + 1);
-            double sx = 0.0, sy = 0.0;
-            for (int j = 0; j < q; ++j) {
-                const double2 uv = u[2 * j];
-                const double v = vr[j];
-                sx = fma(v, uv.x, sx);
-                sy = fma(v, uv.y, sy);
-            }
-            Us[((pp * 2 + part) * 4 + side) * SP_T + r] = make_double2(sx, sy);
-        }
-        __syncthreads();
         const double2* Db = Ds + buf * SP_PB * SP_T * SP_T;
         const double2* dEb = dEs + buf * SP_PB * 4;
         if (act) {
@@ -333,9 +306,8 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
                     const double2 d0 = dEb[pp * 4 + 0], d1 = dEb[pp * 4 + 1], d2 = dEb[pp * 4 + 2];
 #pragma unroll
                     for (int part = 0; part < 2; ++part) {
-                        const double2* U = Us + (pp * 2 + part) * 4 * SP_T;
-                        const double2 ubv = U[0 * SP_T + ip], ur = U[1 * SP_T + jp];
-                        const double2 ut = U[2 * SP_T + ip], ul = U[3 * SP_T + jp];
+                        const double2* U = ub + (pp * 2 + part) * SP_NB;   // [bottom | right | top | left]
+                        const double2 ubv = U[ip], ur = U[q + jp], ut = U[2 * q + ip], ul = U[3 * q + jp];
                         const double bx = a0i * ul.x + a1i * ur.x + ubv.x * a0j + ut.x * a1j;
                         const double by = a0i * ul.y + a1i * ur.y + ubv.y * a0j + ut.y * a1j;
                         // t = -c2 Dinv b
@@ -349,7 +321,7 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
         }
         if (eact) {
             for (int pp = 0; pp < nbat; ++pp) {
-                const double2 u = ub[pp * 2 * nbnd + t];
+                const double2 u = ub[(pp * 2 + e_part) * SP_NB + e_b];
 #pragma unroll
                 for (int kk = 0; kk < 3; ++kk) {
                     const double2 de = dEb[pp * 4 + kk];
@@ -357,10 +329,9 @@ __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
                 }
             }
         }
-        // stage the prefetched batch; Us and UBs[buf] are rewritten after the barrier
+        // stage the prefetched batch into the other buffers (read after the barrier)
         if (more) {
-#pragma unroll
-            for (int u = 0; u < SP_UBR; ++u) UBs[(buf ^ 1) * SP_UBN + t + u * SP_THREADS] = pre[u];
+            sp_stage_ub(pre, nbnd, UBs + (buf ^ 1) * SP_UBN);
             if (t < 4 * SP_PB) dEs[(buf ^ 1) * SP_PB * 4 + t] = pde;
         }
         cp_async_wait_all();
@@ -388,10 +359,12 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
     __shared__ double es[3][SP_T * SP_T];
     __shared__ double ts[3][SP_T * SP_T];
     __shared__ double vs[SP_T * (SP_T + 1)];
+    __shared__ double eb[3][SP_NB];
     const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
     const int leaf = blockIdx.x / a.R2, r2 = blockIdx.x % a.R2;
     const size_t NIs = (size_t)a.nelem * q2;
     for (int e = t; e < SP_T * SP_T; e += blockDim.x) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
+    __syncthreads();
     for (int e = t; e < a.nE * q2; e += blockDim.x) {
         const int kk = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
         const double* src = a.Ehat + ((size_t)kk * a.R2 + r2) * NIs + (size_t)leaf * q2 + mode;
@@ -402,16 +375,26 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
         for (int f = 0; f < a.nF; ++f) s += a.Pi[((size_t)kk * a.nF + f) * SP_T * SP_T + ip * SP_T + jp] * G[(size_t)f * q2];
         es[kk][mode] = s;   // E^[i'][j'] at j'*q + i'
     }
+    // owned edge segments: sum over groups (into shared memory), then back from
+    // the edge basis, E = V E' per segment (after the barrier below)
+    for (int e = t; e < a.nE * nbnd; e += blockDim.x) {
+        const int kk = e / nbnd, b = e % nbnd;
+        double s = 0.0;
+        if (a.own[(size_t)leaf * nbnd + b]) {
+            const double* src = a.Eedge + ((size_t)kk * a.R2 + r2) * a.NE + a.gB[(size_t)leaf * nbnd + b];
+            for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.R2 * a.NE];
+        }
+        eb[kk][b] = s;
+    }
+    __syncthreads();
     for (int e = t; e < a.nE * nbnd; e += blockDim.x) {
         const int kk = e / nbnd, b = e % nbnd;
         if (!a.own[(size_t)leaf * nbnd + b]) continue;
-        const int ge = a.gB[(size_t)leaf * nbnd + b];
-        const double* src = a.Eedge + ((size_t)kk * a.R2 + r2) * a.NE + ge;
+        const int side = b / q, s1 = b % q;
         double s = 0.0;
-        for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.R2 * a.NE];
-        a.E[((size_t)kk * a.R2 + r2) * a.N + (a.N - a.NE) + ge] = s;
+        for (int kq = 0; kq < q; ++kq) s = fma(vs[s1 * (SP_T + 1) + kq], eb[kk][side * q + kq], s);
+        a.E[((size_t)kk * a.R2 + r2) * a.N + (a.N - a.NE) + a.gB[(size_t)leaf * nbnd + b]] = s;
     }
-    __syncthreads();
     // T1[(j', i)] = sum_i' V[i][i'] E^[i'][j']
     for (int e = t; e < a.nE * q2; e += blockDim.x) {
         const int kk = e / q2, node = e % q2, i = node % q, jp = node / q;

@@ -15,6 +15,7 @@ struct StageCfg {
     int kind = 0;   // 0: DMMA GEMM (k_cgemm), 1: GEMV (k_gemv)
     int MT = 4, WN = 8;
     int minb = 1;   // 4: register-capped variant (4 resident CTAs per SM)
+    int rb = 64;    // GEMV row block (CS = 256 / rb column groups)
 };
 
 struct Level {

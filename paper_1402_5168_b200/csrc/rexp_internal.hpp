@@ -119,6 +119,9 @@ int real_eig(int q, const std::vector<double>& K, std::vector<double>& lam, std:
 // root_fourier (shared store only): the periodic closure as n Fourier blocks
 // (ops.back().m[1], [half][n][2q x 2q]) instead of the dense ns x ns inverse (m[0])
 int factor_host(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1,
-                bool shared, int nthreads, std::vector<HostLevelOps>& ops, bool root_fourier = false);
+                bool shared, int nthreads, std::vector<HostLevelOps>& ops, bool root_fourier = false,
+                bool edge_basis = false);
+// edge_basis (with root_fourier): stored merge / root operators act on edge
+// data in the spectral basis V^-1 u of every q-node edge segment
 
 }  // namespace rexp

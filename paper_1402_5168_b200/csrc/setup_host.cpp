@@ -151,6 +151,32 @@ bool zinverse(int n, cd* A) {
 }
 
 // store row-major (rows x cols) as column-major into dst
+// M (rows x cols, row-major) <- Vb^-1 M Vb with Vb = blockdiag(V) over q-row and
+// q-column segments (rows, cols multiples of q)
+void conj_edge_basis(std::vector<cd>& M, int rows, int cols, int q, const std::vector<double>& V,
+                     const std::vector<double>& Vi) {
+    std::vector<cd> tmp(static_cast<size_t>(q));
+    for (int c = 0; c < cols; ++c)
+        for (int s0 = 0; s0 < rows; s0 += q) {
+            for (int a = 0; a < q; ++a) {
+                cd acc = 0.0;
+                for (int b = 0; b < q; ++b) acc += Vi[static_cast<size_t>(a) * q + b] * M[static_cast<size_t>(s0 + b) * cols + c];
+                tmp[a] = acc;
+            }
+            for (int a = 0; a < q; ++a) M[static_cast<size_t>(s0 + a) * cols + c] = tmp[a];
+        }
+    for (int r = 0; r < rows; ++r)
+        for (int s0 = 0; s0 < cols; s0 += q) {
+            cd* row = M.data() + static_cast<size_t>(r) * cols + s0;
+            for (int a = 0; a < q; ++a) {
+                cd acc = 0.0;
+                for (int b = 0; b < q; ++b) acc += row[b] * V[static_cast<size_t>(b) * q + a];
+                tmp[a] = acc;
+            }
+            for (int a = 0; a < q; ++a) row[a] = tmp[a];
+        }
+}
+
 void store_colmajor(const cd* src, int rows, int cols, cd* dst) {
     for (int c = 0; c < cols; ++c)
         for (int r = 0; r < rows; ++r) dst[static_cast<size_t>(c) * rows + r] = src[static_cast<size_t>(r) * cols + c];
@@ -242,6 +268,12 @@ struct Ctx {
     LeafGeom lg;
     bool shared;
     bool root_fourier;
+    // spectral edge basis (shared RSW store with the spectral leaf path): every
+    // stored edge operator is conjugated by Vb = blockdiag(V) over its q-node
+    // segments, K = D2[1..q][1..q] = V diag(l) V^-1 (DESIGN.md §6 "edge basis")
+    bool edge_basis;
+    std::vector<double> V, Vi;   // q x q row-major
+
     int h0;
     std::vector<HostLevelOps>* ops;
 };
@@ -339,6 +371,12 @@ int factor_one(const Ctx& C, int hidx) {
             zgemm(ne, ne, n3, cd(1.0), Y.data(), Sm.data(), cd(1.0), Tp.data());
             Tpar[node] = std::move(Tp);
             const size_t base = static_cast<size_t>(slot) * LO.nodes_stored + node;
+            if (C.edge_basis) {   // stored copies only: T above used the nodal operators
+                const int q = T.q;
+                conj_edge_basis(X, n3, n3, q, C.V, C.Vi);
+                conj_edge_basis(Y, ne, n3, q, C.V, C.Vi);
+                conj_edge_basis(Sm, n3, ne, q, C.V, C.Vi);
+            }
             store_colmajor(X.data(), n3, n3, LO.m[0].data() + base * n3 * n3);
             store_colmajor(Y.data(), ne, n3, LO.m[1].data() + base * ne * n3);
             store_colmajor(Sm.data(), n3, ne, LO.m[2].data() + base * n3 * ne);
@@ -394,6 +432,7 @@ int factor_one(const Ctx& C, int hidx) {
                     return REXP_ESINGULAR;
                 }
                 for (auto& v : Mk) v = -v;
+                if (C.edge_basis) conj_edge_basis(Mk, r2q, r2q, q, C.V, C.Vi);
                 store_colmajor(Mk.data(), r2q, r2q,
                                LR.m[1].data() + (static_cast<size_t>(slot) * n + k) * r2q * r2q);
             }
@@ -412,11 +451,19 @@ int factor_one(const Ctx& C, int hidx) {
 }  // namespace
 
 int factor_host(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1, bool shared,
-                int nthreads, std::vector<HostLevelOps>& ops, bool root_fourier) {
+                int nthreads, std::vector<HostLevelOps>& ops, bool root_fourier, bool edge_basis) {
     const int nh = h1 - h0;
     const Cheb ch = make_cheb(T.p);
     root_fourier = root_fourier && shared;
-    Ctx C{&P, &T, &pt, make_leaf_geom(ch, T.n), shared, root_fourier, h0, &ops};
+    Ctx C{&P, &T, &pt, make_leaf_geom(ch, T.n), shared, root_fourier, edge_basis && root_fourier, {}, {}, h0, &ops};
+    if (C.edge_basis) {
+        const int q = T.q;
+        std::vector<double> K(static_cast<size_t>(q) * q), lam;
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j) K[static_cast<size_t>(i) * q + j] = ch.D2[(i + 1) * T.p + (j + 1)];
+        const int rc = real_eig(q, K, lam, C.V, C.Vi);
+        if (rc != REXP_OK) return rc;
+    }
     const int q2 = C.lg.q2, nb = C.lg.nb;
     // allocate
     ops.assign(T.levels.size() + 2, HostLevelOps());
