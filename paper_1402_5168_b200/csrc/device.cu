@@ -724,6 +724,9 @@ int pick_nb(int nodes, int R2, bool shared) {
 DeviceStore::~DeviceStore() { release(); }
 
 void DeviceStore::release() {
+    drop_graph();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    cap_stream = nullptr;
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
     for (auto e : tpool) cudaEventDestroy(e);
@@ -1020,6 +1023,10 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     }
     if ((rc = walloc(&d_E, static_cast<size_t>(nE) * R2 * N, 8))) return rc;
     if ((rc = walloc(&d_u, static_cast<size_t>(nrhs) * 3 * N * 2, 8))) return rc;
+    {
+        const char* env = std::getenv("REXP_GRAPH");
+        use_graph = !(env && std::string(env) == "0");
+    }
     configure_kernels();
     return tune_stages(false);
 }
@@ -1367,6 +1374,7 @@ int DeviceStore::tune_stages(bool measure) {
     if (!shared) tune(3, 0, t_root);
     timing = saved_timing;
     tuned = true;
+    drop_graph();   // stage choices changed
     if (flush) cudaFree(flush);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1554,10 +1562,47 @@ int DeviceStore::recover(const double* d_E_in, double* d_state, cudaStream_t s) 
     return check("recover");
 }
 
-int DeviceStore::step(double* d_state, cudaStream_t s) {
+int DeviceStore::step_eager(double* d_state, cudaStream_t s) {
     int rc = solve_sum(d_state, d_E, s);
     if (rc) return rc;
     return recover(d_E, d_state, s);
+}
+
+void DeviceStore::drop_graph() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    graph_exec = nullptr;
+    graph_state = nullptr;
+}
+
+// One step as a CUDA graph: the ~2 + 2 L + 4 launches of a step are captured
+// once (on a private stream: the legacy default stream cannot be captured) and
+// replayed on the caller's stream, removing the inter-kernel launch gaps.
+// Per-kernel timing (timing_begin) and REXP_GRAPH=0 use the eager launches.
+int DeviceStore::step(double* d_state, cudaStream_t s) {
+    if (timing || !use_graph) return step_eager(d_state, s);
+    if (!graph_exec || graph_state != d_state) {
+        drop_graph();
+        if (!cap_stream && cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+            return check("graph stream");
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+            return check("graph capture");
+        const int rc = step_eager(d_state, cap_stream);
+        const cudaError_t ce = cudaStreamEndCapture(cap_stream, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (ce != cudaSuccess || cudaGraphInstantiate(&graph_exec, g, 0) != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            graph_exec = nullptr;
+            return check("graph instantiate");
+        }
+        cudaGraphDestroy(g);
+        graph_state = d_state;
+    }
+    if (cudaGraphLaunch(graph_exec, s) != cudaSuccess) return check("graph launch");
+    return REXP_OK;
 }
 
 

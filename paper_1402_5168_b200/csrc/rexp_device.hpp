@@ -34,8 +34,11 @@ class DeviceStore {
     int init(const Problem& P, const Tree& T, const PoleTables& pt, int h0, int h1, bool shared, int nrhs);
     int upload_ops(const std::vector<HostLevelOps>& ops, int m0);
     void release();
-    // one full step on a device state [nrhs][3][N] complex128
+    // one full step on a device state [nrhs][3][N] complex128 (CUDA graph replay
+    // unless timing or REXP_GRAPH=0; step_eager launches the kernels directly)
     int step(double* d_state, cudaStream_t s);
+    int step_eager(double* d_state, cudaStream_t s);
+    bool use_graph = true;
     // all half poles of the handle, chunk by chunk: leaf solves, merge sweeps and
     // the weighted pole sums E (written to d_E_out)
     int solve_sum(const double* d_state, double* d_E_out, cudaStream_t s);
@@ -77,6 +80,10 @@ class DeviceStore {
     cudaEvent_t next_event();
 
     std::vector<void*> allocs;
+    cudaGraphExec_t graph_exec = nullptr;
+    const double* graph_state = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    void drop_graph();
     double *d_D = nullptr, *d_Dw = nullptr, *d_kappa = nullptr, *d_NI = nullptr, *d_F = nullptr;
     int *d_elem_g = nullptr, *d_leaf_gB = nullptr, *d_rpos1 = nullptr, *d_rpos2 = nullptr, *d_rgs = nullptr;
     double2 *d_cF = nullptr, *d_dE = nullptr, *d_Dinv = nullptr;
