@@ -723,10 +723,26 @@ int pick_nb(int nodes, int R2, bool shared) {
 
 DeviceStore::~DeviceStore() { release(); }
 
+void DeviceStore::use_lane(int ln) {
+    LaneBufs& B = lane_bufs[ln];
+    d_edge = B.edge;
+    d_h[0] = B.h[0];
+    d_h[1] = B.h[1];
+    for (size_t li = 0; li < levels.size(); ++li) levels[li].w3 = B.w3[li];
+    cur_lane = ln;
+}
+
 void DeviceStore::release() {
     drop_graph();
     if (cap_stream) cudaStreamDestroy(cap_stream);
     cap_stream = nullptr;
+    for (auto& B : lane_bufs) {
+        if (B.stream) cudaStreamDestroy(B.stream);
+        if (B.done) cudaEventDestroy(B.done);
+    }
+    lane_bufs.clear();
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    ev_fork = nullptr;
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
     for (auto e : tpool) cudaEventDestroy(e);
@@ -985,11 +1001,20 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     for (auto& D : levels) w3_per_pole += static_cast<size_t>(D.nodes) * D.n3;
     // the spectral leaf path never forms the per-pole interior solutions
     const size_t per_pole = ((fdm ? 0 : static_cast<size_t>(NI)) + NE + 2 * hmax + w3_per_pole) * R2 * 16;
+    // pole lanes (spectral path): the half poles are split into nlanes contiguous
+    // ranges whose trees run on separate streams (HBM-bound top levels of one
+    // lane overlap the latency-bound low levels / leaves of the other);
+    // REXP_LANES overrides, the per-node path uses one lane
+    {
+        const char* env = std::getenv("REXP_LANES");
+        nlanes = fdm ? (env ? std::atoi(env) : 2) : 1;
+        nlanes = std::max(1, std::min(nlanes, std::min(nh, 4)));
+    }
     {
         size_t budget = static_cast<size_t>(16) << 30;   // 16 GiB of per-pole work buffers
         const char* env = std::getenv("REXP_CHUNK");
-        chunk = env ? std::max(1, std::atoi(env)) : static_cast<int>(std::max<size_t>(1, budget / per_pole));
-        chunk = std::min(chunk, nh);
+        chunk = env ? std::max(1, std::atoi(env)) : static_cast<int>(std::max<size_t>(1, budget / per_pole / nlanes));
+        chunk = std::min(chunk, nh / nlanes);   // every lane's first chunk is full
     }
     {
         int dev = 0;
@@ -1011,16 +1036,30 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         ngroups = env ? std::atoi(env) : static_cast<int>((16LL * num_sms + ctas - 1) / ctas);
         ngroups = std::max(1, std::min(ngroups, chunk));
         if ((rc = walloc(&d_G, static_cast<size_t>(nelem) * R2 * nF * q2, 8))) return rc;
-        if ((rc = walloc(&d_Ehat, static_cast<size_t>(ngroups) * nE * R2 * NI, 8))) return rc;
-        if ((rc = walloc(&d_Eedge, static_cast<size_t>(ngroups) * nE * R2 * NE, 8))) return rc;
+        // partial slots [lane][group]
+        if ((rc = walloc(&d_Ehat, static_cast<size_t>(nlanes) * ngroups * nE * R2 * NI, 8))) return rc;
+        if ((rc = walloc(&d_Eedge, static_cast<size_t>(nlanes) * ngroups * nE * R2 * NE, 8))) return rc;
     }
-    if ((rc = walloc(&d_edge, pc * NE * R2, 16))) return rc;
-    if ((rc = walloc(&d_h[0], pc * hmax * R2, 16))) return rc;
-    if ((rc = walloc(&d_h[1], pc * hmax * R2, 16))) return rc;
-    for (size_t li = 0; li < levels.size(); ++li) {
-        Level& D = levels[li];
-        if ((rc = walloc(&D.w3, pc * D.nodes * D.n3 * R2, 16))) return rc;
+    lane_bufs.assign(nlanes, LaneBufs());
+    for (int ln = 0; ln < nlanes; ++ln) {
+        LaneBufs& B = lane_bufs[ln];
+        if ((rc = walloc(&B.edge, pc * NE * R2, 16))) return rc;
+        if ((rc = walloc(&B.h[0], pc * hmax * R2, 16))) return rc;
+        if ((rc = walloc(&B.h[1], pc * hmax * R2, 16))) return rc;
+        B.w3.assign(levels.size(), nullptr);
+        for (size_t li = 0; li < levels.size(); ++li)
+            if ((rc = walloc(&B.w3[li], pc * levels[li].nodes * levels[li].n3 * R2, 16))) return rc;
+        B.m0 = static_cast<int>(static_cast<long long>(nh) * ln / nlanes);
+        B.m1 = static_cast<int>(static_cast<long long>(nh) * (ln + 1) / nlanes);
+        if (nlanes > 1) {
+            if (cudaStreamCreateWithFlags(&B.stream, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&B.done, cudaEventDisableTiming) != cudaSuccess)
+                return check("lane streams");
+        }
     }
+    if (nlanes > 1 && cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess)
+        return check("lane fork event");
+    use_lane(0);
     if ((rc = walloc(&d_E, static_cast<size_t>(nE) * R2 * N, 8))) return rc;
     if ((rc = walloc(&d_u, static_cast<size_t>(nrhs) * 3 * N * 2, 8))) return rc;
     {
@@ -1172,7 +1211,8 @@ void DeviceStore::configure_kernels() {
 }
 
 int DeviceStore::launches_per_step() const {
-    const int nchunks = (nh + chunk - 1) / chunk;
+    int nchunks = 0;
+    for (const auto& B : lane_bufs) nchunks += (B.m1 - B.m0 + chunk - 1) / chunk;
     const int per_chunk = (shared && !fdm ? 5 : 4) + 3 * static_cast<int>(levels.size());
     return fdm ? 4 + nchunks * (3 + 3 * static_cast<int>(levels.size())) : 2 + nchunks * per_chunk;
 }
@@ -1495,11 +1535,15 @@ SpecArgs DeviceStore::spec_args(int m0, int pc) const {
     sp.dE = d_dE + static_cast<size_t>(m0) * nE;
     sp.F = d_F; sp.G = d_G;
     sp.q = q; sp.p = p; sp.nF = nF; sp.nE = nE; sp.nelem = nelem; sp.R2 = R2; sp.nh = pc;
-    sp.ngroups = std::min(ngroups, pc); sp.accumulate = m0 > 0 ? 1 : 0;
+    sp.ngroups = std::min(ngroups, pc);
+    sp.accumulate = m0 > lane_bufs[cur_lane].m0 ? 1 : 0;
     sp.c1 = c1; sp.c2 = c1 * c1;
     sp.h = d_h[0]; sp.hps = hstride;
     sp.edge = d_edge; sp.NE = NE; sp.gB = d_leaf_gB; sp.own = d_leaf_own;
-    sp.Ehat = d_Ehat; sp.Eedge = d_Eedge; sp.Pi = d_Pi; sp.E = nullptr; sp.N = N;
+    // this lane's partial slots (k_spec_back sums every lane's)
+    sp.Ehat = d_Ehat + static_cast<size_t>(cur_lane) * ngroups * nE * R2 * NI;
+    sp.Eedge = d_Eedge + static_cast<size_t>(cur_lane) * ngroups * nE * R2 * NE;
+    sp.Pi = d_Pi; sp.E = nullptr; sp.N = N;
     return sp;
 }
 
@@ -1533,13 +1577,31 @@ int DeviceStore::solve_sum(const double* d_state, double* d_E_out, cudaStream_t 
         tend(T_PRE, s);
     }
     int rc;
-    for (int m0 = 0; m0 < nh; m0 += chunk) {
-        const int pc = std::min(chunk, nh - m0);
-        if ((rc = tree_chunk(m0, pc, s))) return rc;
-        if (!fdm && (rc = pole_sum_chunk(m0, pc, m0 > 0, d_E_out, s))) return rc;
+    // lanes: concurrent streams forked from s (captured into the step graph);
+    // per-kernel timing runs them one after the other on s
+    const bool fork = nlanes > 1 && !timing;
+    if (fork) cudaEventRecord(ev_fork, s);
+    for (int ln = 0; ln < nlanes; ++ln) {
+        use_lane(ln);
+        const LaneBufs& B = lane_bufs[ln];
+        cudaStream_t ls = fork ? B.stream : s;
+        if (fork) cudaStreamWaitEvent(ls, ev_fork, 0);
+        for (int m0 = B.m0; m0 < B.m1; m0 += chunk) {
+            const int pc = std::min(chunk, B.m1 - m0);
+            if ((rc = tree_chunk(m0, pc, ls))) return rc;
+            if (!fdm && (rc = pole_sum_chunk(m0, pc, m0 > 0, d_E_out, ls))) return rc;
+        }
+        if (fork) {
+            cudaEventRecord(B.done, ls);
+            cudaStreamWaitEvent(s, B.done, 0);
+        }
     }
+    use_lane(0);
     if (fdm) {
         SpecArgs sp = spec_args(0, chunk);
+        sp.ngroups = nlanes * std::min(ngroups, chunk);   // every lane's slots
+        sp.Ehat = d_Ehat;
+        sp.Eedge = d_Eedge;
         sp.E = d_E_out;
         tbeg(s);
         k_spec_back<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);

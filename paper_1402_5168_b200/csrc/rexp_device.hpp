@@ -80,6 +80,19 @@ class DeviceStore {
     cudaEvent_t next_event();
 
     std::vector<void*> allocs;
+    // pole lanes: per-lane work buffers, pole range and stream (see init)
+    struct LaneBufs {
+        double2* edge = nullptr;
+        double2* h[2] = {nullptr, nullptr};
+        std::vector<double2*> w3;
+        int m0 = 0, m1 = 0;
+        cudaStream_t stream = nullptr;
+        cudaEvent_t done = nullptr;
+    };
+    std::vector<LaneBufs> lane_bufs;
+    int nlanes = 1, cur_lane = 0;
+    cudaEvent_t ev_fork = nullptr;
+    void use_lane(int ln);
     cudaGraphExec_t graph_exec = nullptr;
     const double* graph_state = nullptr;
     cudaStream_t cap_stream = nullptr;
