@@ -39,7 +39,15 @@ struct CgemmArgs {
     long long add_ps;
     const int* ai0;         // UPY: [nodes][rows] ext index into add
     const int* so0;         // DOWN: [nodes][rows] scatter index
+    // UPX / UPY gathers are affine in the node (mesh.cpp): index(node, k) =
+    // ca(node) * nchild + index(0, k), ca(node) = 2 node (x-merge) or
+    // node + (node / nbx) nbx (y-merge); only node 0's rows (bi0, bi1, ai0) are read
+    int nbx, xdir, nchild;
 };
+
+__device__ __forceinline__ int cg_child_base(const CgemmArgs& a, int node) {
+    return (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
+}
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -71,9 +79,9 @@ __device__ __forceinline__ void cg_fetch(const CgemmArgs& a, int m, int k, int c
     } else if (MODE == CG_UPX || MODE == CG_ROOT) {
         // ROOT: one node, node-independent seam positions pos1/pos2 (P^T h)
         const double2* s = a.src + (size_t)m * a.src_ps * R2;
-        const size_t o = MODE == CG_ROOT ? (size_t)k : (size_t)node * a.K + k;
-        const double2 v0 = s[(size_t)a.bi0[o] * R2 + r2];
-        const double2 v1 = s[(size_t)a.bi1[o] * R2 + r2];
+        const int base = MODE == CG_ROOT ? 0 : cg_child_base(a, node);
+        const double2 v0 = s[(size_t)(base + a.bi0[k]) * R2 + r2];
+        const double2 v1 = s[(size_t)(base + a.bi1[k]) * R2 + r2];
         r.v[0] = v0.x; r.v[1] = v0.y; r.v[2] = v1.x; r.v[3] = v1.y;
     } else if (MODE == CG_UPY) {
         const double2 v = a.src[(size_t)m * a.src_ps * R2 + ((size_t)node * a.K + k) * R2 + r2];
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
                         if (MODE == CG_LEAF_DOWN)
                             addv[i][n][j] = a.dst[(((size_t)m * a.nodes + node) * a.rows + row) * R2 + r2];
                         else if (MODE == CG_UPY)
-                            addv[i][n][j] = a.add[((size_t)m * a.add_ps + a.ai0[(size_t)node * a.rows + row]) * R2 + r2];
+                            addv[i][n][j] = a.add[((size_t)m * a.add_ps + cg_child_base(a, node) + a.ai0[row]) * R2 + r2];
                         else
                             addv[i][n][j] = a.add[(size_t)m * a.add_ps * R2 + ((size_t)node * a.rows + row) * R2 + r2];
                     }

@@ -268,6 +268,9 @@ struct GemvArgs {
     double2* ydst;          // destination
     long long ydst_ps;
     const int* yo;          // ROOT/DOWN: scatter index [nodes][rows] or [rows]
+    // UPX / UPY gathers are affine in the node: index(node, k) = child base +
+    // index(0, k) (see CgemmArgs)
+    int nbx, xdir, nchild;
 };
 
 template <int R2, int NB, int MODE>
@@ -289,8 +292,9 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
         const int node = node0 + nb;
         double2 v;
         if (MODE == MODE_UPX) {
-            const double2 v0 = src[(size_t)a.xi0[(size_t)node * cols + c] * R2 + r2];
-            const double2 v1 = src[(size_t)a.xi1[(size_t)node * cols + c] * R2 + r2];
+            const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
+            const double2 v0 = src[(size_t)(base + a.xi0[c]) * R2 + r2];
+            const double2 v1 = src[(size_t)(base + a.xi1[c]) * R2 + r2];
             v = make_double2(v0.x + v1.x, v0.y + v1.y);
         } else if (MODE == MODE_UPY) {
             v = src[((size_t)node * cols + c) * R2 + r2];
@@ -367,7 +371,8 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
             if (MODE == MODE_UPX) {
                 dst[((size_t)node * rows + row) * R2 + r] = v;
             } else if (MODE == MODE_UPY) {
-                const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + (size_t)a.yi[(size_t)node * rows + row] * R2 + r];
+                const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
+                const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + (size_t)(base + a.yi[row]) * R2 + r];
                 v.x += add.x;
                 v.y += add.y;
                 dst[((size_t)node * rows + row) * R2 + r] = v;
@@ -970,6 +975,7 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         const MergeLevel& L = T.levels[li];
         Level& D = levels[li];
         D.nodes = L.nodes; D.n3 = L.n3; D.next = L.next; D.nchild = L.nchild; D.child_nodes = L.child_nodes;
+        D.nbx = L.nbx; D.dir = L.dir;
         const size_t st = shared ? 1 : static_cast<size_t>(L.nodes);
         D.ppX = st * L.n3 * L.n3;
         D.ppY = st * L.next * L.n3;
@@ -1274,6 +1280,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     if (cfg.kind == 0) {
         CgemmArgs a{};
         a.nodes = L.nodes; a.R2 = R2;
+        a.nbx = L.nbx; a.xdir = L.dir == 0 ? 1 : 0; a.nchild = L.nchild;
         int mode;
         if (kind == 0) {
             mode = CG_UPX;
@@ -1317,6 +1324,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
         g.ysrc = L.w3; g.ysrc_ps = static_cast<long long>(L.nodes) * L.n3;
         g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
     }
+    g.nbx = L.nbx; g.xdir = L.dir == 0 ? 1 : 0; g.nchild = L.nchild;
     const dim3 grid((L.nodes / NB) * g.nrowblk, pc);
     const size_t smem = gemv_smem(g, NB, R2);
     tbeg(s);

@@ -19,7 +19,7 @@ struct StageCfg {
 };
 
 struct Level {
-    int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0;
+    int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0, nbx = 1, dir = 0;
     double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
     int *ia3 = nullptr, *ib3 = nullptr, *ext = nullptr, *gext = nullptr, *g3 = nullptr;
     double2* w3 = nullptr;                              // [chunk][nodes][n3][R2]

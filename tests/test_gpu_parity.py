@@ -104,6 +104,30 @@ def test_config0_many_rhs_and_pole_chunks(c0, nrhs, chunk, monkeypatch):
     h.close()
 
 
+@pytest.mark.parametrize("lanes,chunk,graph", [("1", "1000", "1"), ("3", "23", "1"), ("2", "1000", "0")])
+def test_config0_lanes_chunks_graph(c0, lanes, chunk, graph, monkeypatch):
+    """Execution modes of the shared store: pole lanes on forked streams
+    (REXP_LANES), pole chunks inside each lane with per-lane accumulation of the
+    spectral pole sums (REXP_CHUNK), CUDA-graph replay vs eager launches
+    (REXP_GRAPH).  Every mode matches the oracle; graph replay and eager
+    launches give identical bits (same kernels, no atomics)."""
+    cfg, m, op, u0 = c0
+    Lam = cfg["Lambda_tau"] / cfg["tau"]
+    monkeypatch.setenv("REXP_LANES", lanes)
+    monkeypatch.setenv("REXP_CHUNK", chunk)
+    monkeypatch.setenv("REXP_GRAPH", graph)
+    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"])
+    got = _gpu_apply(h, u0, 3)
+    err = rel_l2(got, op.evolve(u0, 3))
+    print(f"lanes {lanes} chunk {chunk} graph {graph}: rel L2 {err:.3e}")
+    assert err <= TOL
+    h.close()
+    monkeypatch.setenv("REXP_GRAPH", "0" if graph == "1" else "1")
+    h2 = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"])
+    assert np.array_equal(_gpu_apply(h2, u0, 3), got)
+    h2.close()
+
+
 def test_edge_cases_zero_state_and_zero_steps(c0):
     cfg, m, op, u0 = c0
     Lam = cfg["Lambda_tau"] / cfg["tau"]

@@ -238,3 +238,27 @@ def test_root_seam_operator_block_circulant(host_rsw):
             for ep in range(n):
                 R[:, e, :, :, ep, :] = Cb[(e - ep) % n].reshape(2, q, 2, q)
         assert np.abs(R.reshape(ns, ns) - X).max() < 1e-11 * scale
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_merge_gather_indices_affine_in_node(n):
+    """The device up-sweep gathers (ia3, ib3, ext) compute index(node, k) as
+    ca(node) * nchild + index(0, k), ca = 2 node (x-merge, including the
+    cylinder) or node + (node // nbx) * nbx (y-merge); check that against the
+    tree builder's full index lists."""
+    from paper_1402_5168_b200 import api
+    h = api.setup("rsw", n=n, p=6, tau=0.2, delta=1e-10, Lambda=100.0, f=1.0, device=-1, store="pernode")
+    nlev = api.export_num_levels(h)
+    ac = bc = 1
+    for lev in range(1, nlev - 1):
+        xdir = (lev - 1) % 2 == 0
+        if xdir:
+            ac *= 2
+        else:
+            bc *= 2
+        nbx = n // ac
+        nodes, _, n3, ne, nc = api.export_level_info(h, lev)[:5]
+        ca = np.array([2 * nd if xdir else nd + (nd // nbx) * nbx for nd in range(nodes)])
+        for which, cnt in ((0, n3), (1, n3), (2, ne)):
+            idx = api.export_index(h, lev, which, nodes * cnt).reshape(nodes, cnt)
+            assert (ca[:, None] * nc + idx[0][None, :] == idx).all()
