@@ -273,6 +273,23 @@ struct GemvArgs {
     int nbx, xdir, nchild;
 };
 
+template <int MODE>
+__device__ __forceinline__ void gemv_epilogue(const GemvArgs& a, int m, int node, int row, int r, int R2, double2 v) {
+    double2* dst = a.ydst + (size_t)m * a.ydst_ps * R2;
+    if (MODE == MODE_UPX) {
+        dst[((size_t)node * a.rows + row) * R2 + r] = v;
+    } else if (MODE == MODE_UPY) {
+        const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
+        const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + (size_t)(base + a.yi[row]) * R2 + r];
+        dst[((size_t)node * a.rows + row) * R2 + r] = make_double2(v.x + add.x, v.y + add.y);
+    } else if (MODE == MODE_ROOT) {
+        dst[(size_t)a.yo[row] * R2 + r] = v;
+    } else {
+        const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + ((size_t)node * a.rows + row) * R2 + r];
+        dst[(size_t)a.yo[(size_t)node * a.rows + row] * R2 + r] = make_double2(v.x + add.x, v.y + add.y);
+    }
+}
+
 template <int R2, int NB, int MODE>
 __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
     extern __shared__ double2 sm[];
@@ -321,16 +338,30 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
         const double2* M = a.M + mat + row;
         const int CS = a.CS;
         int c = cs;
-        for (; c + 7 * CS < cols; c += 8 * CS) {
-            double2 mv[8];
+        // software pipelined: the next 8 column loads are issued before the
+        // current 8 are used, so the operator stream never drains
+        if (c + 7 * CS < cols) {
+            double2 mv[8], nx[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) mv[u] = ldg2(M + (size_t)(c + u * CS) * rows);
+            for (;;) {
+                const int cn = c + 8 * CS;
+                const bool more = cn + 7 * CS < cols;
+                if (more) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+                    for (int u = 0; u < 8; ++u) nx[u] = ldg2(M + (size_t)(cn + u * CS) * rows);
+                }
 #pragma unroll
-                for (int nb = 0; nb < NB; ++nb)
+                for (int u = 0; u < 8; ++u)
 #pragma unroll
-                    for (int r = 0; r < R2; ++r) cfma(acc[nb][r], mv[u], xs[(nb * cols + c + u * CS) * R2 + r]);
+                    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                        for (int r = 0; r < R2; ++r) cfma(acc[nb][r], mv[u], xs[(nb * cols + c + u * CS) * R2 + r]);
+                c = cn;
+                if (!more) break;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) mv[u] = nx[u];
+            }
         }
         for (; c < cols; c += CS) {
             const double2 mv = ldg2(M + (size_t)c * rows);
@@ -361,31 +392,10 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
         }
     }
     if (cs != 0 || row >= rows) return;
-    double2* dst = a.ydst + (size_t)m * a.ydst_ps * R2;
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-        const int node = node0 + nb;
+    for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-        for (int r = 0; r < R2; ++r) {
-            double2 v = acc[nb][r];
-            if (MODE == MODE_UPX) {
-                dst[((size_t)node * rows + row) * R2 + r] = v;
-            } else if (MODE == MODE_UPY) {
-                const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
-                const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + (size_t)(base + a.yi[row]) * R2 + r];
-                v.x += add.x;
-                v.y += add.y;
-                dst[((size_t)node * rows + row) * R2 + r] = v;
-            } else if (MODE == MODE_ROOT) {
-                dst[(size_t)a.yo[row] * R2 + r] = v;
-            } else {
-                const double2 add = a.ysrc[(size_t)m * a.ysrc_ps * R2 + ((size_t)node * rows + row) * R2 + r];
-                v.x += add.x;
-                v.y += add.y;
-                dst[(size_t)a.yo[(size_t)node * rows + row] * R2 + r] = v;
-            }
-        }
-    }
+        for (int r = 0; r < R2; ++r) gemv_epilogue<MODE>(a, m, node0 + nb, row, r, R2, acc[nb][r]);
 }
 
 // --------------------------------------------------------------------------
