@@ -72,6 +72,7 @@ __global__ void k_pre(PreArgs a) {
     auto val = [&](int fld, int node) { return base[((size_t)fld * a.N + node) * 2]; };
     // derivatives along the element row j (x) and column i (y)
     double dx0 = 0, dx1 = 0, dy0 = 0, dy1 = 0;
+#pragma unroll 8
     for (int kk = 0; kk < p; ++kk) {
         const double dxw = a.D[i * p + kk], dyw = a.D[j * p + kk];
         const int gx = eg[j * p + kk], gy = eg[kk * p + i];
@@ -634,6 +635,7 @@ __device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, 
         const int i = rr % q + 1, j = rr / q + 1;
         const int* eg = a.elem_g + (size_t)e * p * p;
         double sx = 0.0, sy = 0.0;
+#pragma unroll 8
         for (int k = 0; k < p; ++k) {
             sx += a.D[i * p + k] * Ef[eg[j * p + k]];
             sy += a.D[j * p + k] * Ef[eg[k * p + i]];
@@ -653,6 +655,7 @@ __device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, 
         const int* eg = E_of(e);
         const int* egL = E_of(eL);
         double sr = 0.0, sl = 0.0;
+#pragma unroll 8
         for (int k = 0; k < p; ++k) {
             sr += a.D[0 * p + k] * Ef[eg[t * p + k]];
             sl += a.D[(p - 1) * p + k] * Ef[egL[t * p + k]];
@@ -660,6 +663,7 @@ __device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, 
         gx = 0.5 * a.c1 * (sr + sl);
         const int eBn = ((ey + n - 1) % n) * n + ex, eTn = ((ey + 1) % n) * n + ex;
         double st = a.Dw[(t - 1) * p + 0] * Ef[a.NI + (long long)eBn * q + (q - 1)];
+#pragma unroll 8
         for (int l = 1; l <= q; ++l) st += a.Dw[(t - 1) * p + l] * Ef[a.NI + (long long)e * q + (l - 1)];
         st += a.Dw[(t - 1) * p + (p - 1)] * Ef[a.NI + (long long)eTn * q + 0];
         gy = a.c1 * st;
@@ -668,6 +672,7 @@ __device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, 
         const int* eg = E_of(e);
         const int* egB = E_of(eB);
         double st_ = 0.0, sb = 0.0;
+#pragma unroll 8
         for (int k = 0; k < p; ++k) {
             st_ += a.D[0 * p + k] * Ef[eg[k * p + t]];
             sb += a.D[(p - 1) * p + k] * Ef[egB[k * p + t]];
@@ -676,6 +681,7 @@ __device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, 
         const int eLn = ey * n + (ex + n - 1) % n, eRn = ey * n + (ex + 1) % n;
         const long long hb = a.NI + a.NV;
         double sx = a.Dw[(t - 1) * p + 0] * Ef[hb + (long long)eLn * q + (q - 1)];
+#pragma unroll 8
         for (int l = 1; l <= q; ++l) sx += a.Dw[(t - 1) * p + l] * Ef[hb + (long long)e * q + (l - 1)];
         sx += a.Dw[(t - 1) * p + (p - 1)] * Ef[hb + (long long)eRn * q + 0];
         gx = a.c1 * sx;
@@ -1049,7 +1055,8 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         // pole groups per leaf CTA: enough CTAs to fill the GPU (REXP_GROUPS overrides)
         const long long ctas = static_cast<long long>(nelem) * nrhs;
         const char* env = std::getenv("REXP_GROUPS");
-        ngroups = env ? std::atoi(env) : static_cast<int>((16LL * num_sms + ctas - 1) / ctas);
+        // (lanes run concurrently: the target is shared between them)
+        ngroups = env ? std::atoi(env) : static_cast<int>((16LL * num_sms + ctas * nlanes - 1) / (ctas * nlanes));
         ngroups = std::max(1, std::min(ngroups, chunk));
         if ((rc = walloc(&d_G, static_cast<size_t>(nelem) * R2 * nF * q2, 8))) return rc;
         // partial slots [lane][group]
