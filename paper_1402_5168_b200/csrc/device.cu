@@ -339,9 +339,20 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
         const double2* M = a.M + mat + row;
         const int CS = a.CS;
         int c = cs;
-        // software pipelined: the next 8 column loads are issued before the
-        // current 8 are used, so the operator stream never drains
-        if (c + 7 * CS < cols) {
+        // NB >= 2 (shared store, top levels): software pipelined, the next 8
+        // column loads are issued before the current 8 are used.  NB = 1
+        // (per-node store): plain 8-deep batches keep registers (occupancy) low.
+        if (NB == 1) {
+            for (; c + 7 * CS < cols; c += 8 * CS) {
+                double2 mv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) mv[u] = ldg2(M + (size_t)(c + u * CS) * rows);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int r = 0; r < R2; ++r) cfma(acc[0][r], mv[u], xs[(c + u * CS) * R2 + r]);
+            }
+        } else if (c + 7 * CS < cols) {
             double2 mv[8], nx[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) mv[u] = ldg2(M + (size_t)(c + u * CS) * rows);
