@@ -1239,6 +1239,7 @@ void DeviceStore::configure_kernels() {
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_spec_down, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_spec_up, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
@@ -1480,7 +1481,7 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     const dim3 sp_grid(static_cast<unsigned>(nelem * nrhs), static_cast<unsigned>(sp.ngroups));
     if (fdm) {
         tbeg(s);
-        k_leaf_spec_up<<<sp_grid, SP_THREADS, 0, s>>>(sp);
+        k_leaf_spec_up<<<sp_grid, SP_THREADS, sp_up_smem(), s>>>(sp);
         tend(T_LEAF_UP, s);
     } else if (shared) {
         CgemmArgs a{};

@@ -117,9 +117,19 @@ __device__ __forceinline__ void sp_load_g(const SpecArgs& a, int leaf, int k, in
 // z_s[r] = sum_i' W[i'][r] e_s[i'] (columns), s = 0, 1, and writes the flux
 //   bottom -c1 y0, top +c1 y1, left -c1 z0, right +c1 z1   (edge basis: no V).
 // --------------------------------------------------------------------------
+__device__ __forceinline__ void sp_fetch_dinv(const SpecArgs& a, int mb, int nbat, double2* dst);
+
+constexpr size_t sp_up_smem() {
+    return (2 * (size_t)SP_PB * SP_T * SP_T + (size_t)SP_PB * 2 * SP_T * SP_LW + 2 * SP_PB * 4) * sizeof(double2) +
+           2 * SP_T * sizeof(double);
+}
+
 __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
-    __shared__ double2 Ws[SP_PB][2][SP_T * SP_LW];  // W[i'][j'] at j'*SP_LW + i'
-    __shared__ double es[2 * SP_T];
+    extern __shared__ double2 usm[];
+    double2* Ds = usm;                                   // [2][SP_PB][256] Dinv rows (cp.async, one batch ahead)
+    double2* Ws = Ds + 2 * SP_PB * SP_T * SP_T;          // [SP_PB][2][SP_T * SP_LW] W[i'][j'] at j'*SP_LW + i'
+    double2* cfs = Ws + SP_PB * 2 * SP_T * SP_LW;        // [2][SP_PB][4] c_mf
+    double* es = reinterpret_cast<double*>(cfs + 2 * SP_PB * 4);
     const int q = a.q, nbnd = 4 * q, t = threadIdx.x;
     const int nrhs = a.R2 / 2;
     const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
@@ -131,25 +141,39 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
     const int wpos = jp * SP_LW + ip;
     double g[2][3];
     if (act) sp_load_g(a, leaf, k, jp * q + ip, g);
+    const int cf_pp = t >> 2, cf_f = t & 3;              // c_mf staging task (t < 4 SP_PB)
+    {
+        const int nb0 = min(SP_PB, m1 - m0);
+        sp_fetch_dinv(a, m0, nb0, Ds);
+        if (t < 4 * SP_PB)
+            cfs[t] = (cf_pp < nb0 && cf_f < a.nF) ? a.cF[(size_t)(m0 + cf_pp) * a.nF + cf_f] : make_double2(0.0, 0.0);
+        cp_async_wait_all();
+    }
     __syncthreads();
-    for (int mb = m0; mb < m1; mb += SP_PB) {
+    int buf = 0;
+    for (int mb = m0; mb < m1; mb += SP_PB, buf ^= 1) {
         const int nbat = min(SP_PB, m1 - mb);
+        const bool more = mb + SP_PB < m1;
+        double2 pcf = make_double2(0.0, 0.0);
+        if (more) {
+            const int nbn = min(SP_PB, m1 - mb - SP_PB);
+            sp_fetch_dinv(a, mb + SP_PB, nbn, Ds + (buf ^ 1) * SP_PB * SP_T * SP_T);
+            if (t < 4 * SP_PB && cf_pp < nbn && cf_f < a.nF) pcf = a.cF[(size_t)(mb + SP_PB + cf_pp) * a.nF + cf_f];
+        }
+        const double2* Db = Ds + buf * SP_PB * SP_T * SP_T;
+        const double2* cb = cfs + buf * SP_PB * 4;
         // W = Dinv_m .* sum_f c_mf G_f
         if (act) {
 #pragma unroll
             for (int pp = 0; pp < SP_PB; ++pp) {
                 if (pp < nbat) {
-                    const int m = mb + pp;
-                    const double2* cf = a.cF + (size_t)m * a.nF;
-                    const double2 c0 = cf[0];
-                    const double2 c1v = a.nF > 1 ? cf[1] : make_double2(0.0, 0.0);
-                    const double2 c2v = a.nF > 2 ? cf[2] : make_double2(0.0, 0.0);
-                    const double2 d = __ldg(a.Dinv + (size_t)m * SP_T * SP_T + t);
+                    const double2 c0 = cb[pp * 4 + 0], c1v = cb[pp * 4 + 1], c2v = cb[pp * 4 + 2];
+                    const double2 d = Db[pp * SP_T * SP_T + t];
 #pragma unroll
                     for (int part = 0; part < 2; ++part) {
                         const double sx = c0.x * g[part][0] + c1v.x * g[part][1] + c2v.x * g[part][2];
                         const double sy = c0.y * g[part][0] + c1v.y * g[part][1] + c2v.y * g[part][2];
-                        Ws[pp][part][wpos] = make_double2(sx * d.x - sy * d.y, sx * d.y + sy * d.x);
+                        Ws[(pp * 2 + part) * SP_T * SP_LW + wpos] = make_double2(sx * d.x - sy * d.y, sx * d.y + sy * d.x);
                     }
                 }
             }
@@ -158,7 +182,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
         for (int task = t; task < nbat * 64; task += blockDim.x) {
             const int pp = task >> 6, part = (task >> 5) & 1, col = (task >> 4) & 1, r = task & 15;
             if (r >= q) continue;
-            const double2* W = Ws[pp][part];
+            const double2* W = Ws + (pp * 2 + part) * SP_T * SP_LW;
             const int base = col ? r * SP_LW : r, step = col ? 1 : SP_LW;
             double s0x = 0.0, s0y = 0.0, s1x = 0.0, s1y = 0.0;
             for (int c = 0; c < q; ++c) {
@@ -172,7 +196,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
             hb[(size_t)(side0 * q + r) * a.R2] = make_double2(-a.c1 * s0x, -a.c1 * s0y);
             hb[(size_t)(side1 * q + r) * a.R2] = make_double2(a.c1 * s1x, a.c1 * s1y);
         }
-        __syncthreads();   // Ws is rewritten by the next batch
+        // stage the next batch's c_mf; Ws / Ds[buf] are rewritten after the barrier
+        if (more && t < 4 * SP_PB) cfs[(buf ^ 1) * SP_PB * 4 + t] = pcf;
+        cp_async_wait_all();
+        __syncthreads();
     }
 }
 
