@@ -175,7 +175,9 @@ def roofline_for(cfg, h, times, steps, pk):
     work = class_work(cfg, nh, R2, shared, leaf=h.leaf_solver or "dense", nF=nF, nE=nE)
     # dominant kernel = the single launch with the largest average duration
     # (the merge tree is many launches of different shapes; it is reported per class)
-    dom = max((k for k in times if times[k][1]), key=lambda k: times[k][0] / times[k][1])
+    # (among the classes with a work model: the per-step pre/recover/pole-sum
+    # kernels are small and bandwidth-trivial)
+    dom = max((k for k in times if times[k][1] and k in work), key=lambda k: times[k][0] / times[k][1])
     ms, nl = times[dom]
     per_launch_ms = ms / max(nl, 1)
     # the spectral leaf kernels run on the FP64 FMA pipe: measured DFMA 35.9 TFLOP/s

@@ -24,7 +24,7 @@ struct CgemmArgs {
     int R2;                 // real right-hand sides per node (used when the template R2 is 0)
     int nrowblk;
     // LEAF_UP
-    const double* F;        // [NI][nF][R2]
+    const double* F;        // [R2][nF][NI]
     const double2* cF;      // [nh][nF]
     int nF, q2;
     // generic gathers
@@ -72,10 +72,11 @@ __device__ __forceinline__ void cg_fetch(const CgemmArgs& a, int m, int k, int c
     const int R2 = R2T ? R2T : a.R2;
     const int node = col / R2, r2 = col % R2;
     if (MODE == CG_LEAF_UP) {
-        const double* f = a.F + ((size_t)(node * a.q2 + k) * a.nF) * R2 + r2;
+        const size_t NI = (size_t)a.nodes * a.q2;
+        const double* f = a.F + (size_t)r2 * a.nF * NI + (size_t)node * a.q2 + k;
         r.v[0] = f[0];
-        r.v[1] = a.nF > 1 ? f[R2] : 0.0;
-        r.v[2] = a.nF > 2 ? f[2 * R2] : 0.0;
+        r.v[1] = a.nF > 1 ? f[NI] : 0.0;
+        r.v[2] = a.nF > 2 ? f[2 * NI] : 0.0;
     } else if (MODE == CG_UPX || MODE == CG_ROOT) {
         // ROOT: one node, node-independent seam positions pos1/pos2 (P^T h)
         const double2* s = a.src + (size_t)m * a.src_ps * R2;

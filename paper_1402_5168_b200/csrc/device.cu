@@ -46,7 +46,7 @@ __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
 // --------------------------------------------------------------------------
 struct PreArgs {
     const double* u;        // state [nrhs][3][N] complex (interleaved)
-    double* F;              // [NI][nF][R2]
+    double* F;              // [R2][nF][NI]
     const int* elem_g;      // [nelem][p*p]
     const double* D;        // p x p
     const double* kappa;    // WAVE: [N]
@@ -56,11 +56,13 @@ struct PreArgs {
 };
 
 __global__ void k_pre(PreArgs a) {
+    // node-fastest threads: neighbouring threads read neighbouring nodes of one
+    // real part and write contiguous F rows
     const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long total = a.NI * a.R2;
     if (tid >= total) return;
-    const int r2 = (int)(tid % a.R2);
-    const long long g = tid / a.R2;
+    const long long g = tid % a.NI;
+    const int r2 = (int)(tid / a.NI);
     const int q2 = a.q * a.q;
     const int e = (int)(g / q2);
     const int rr = (int)(g % q2);
@@ -82,14 +84,14 @@ __global__ void k_pre(PreArgs a) {
         dy1 += dyw * val(1, gy);
     }
     dx0 *= a.c1; dx1 *= a.c1; dy0 *= a.c1; dy1 *= a.c1;
-    double* out = a.F + ((size_t)g * a.nF) * a.R2 + r2;
+    double* out = a.F + (size_t)r2 * a.nF * a.NI + g;
     if (a.model == 0) {  // RSW fields (v1, v2, eta): eta0, div v0, curl v0
         out[0] = val(2, (int)g);
-        out[a.R2] = dx0 + dy1;
-        out[2 * a.R2] = dx1 - dy0;
+        out[a.NI] = dx0 + dy1;
+        out[2 * a.NI] = dx1 - dy0;
     } else {             // WAVE fields (w, z, v): v0/kappa, d_x w0 + d_y z0
         out[0] = val(2, (int)g) / a.kappa[g];
-        out[a.R2] = dx0 + dy1;
+        out[a.NI] = dx0 + dy1;
     }
 }
 
@@ -98,7 +100,7 @@ __global__ void k_pre(PreArgs a) {
 // --------------------------------------------------------------------------
 struct LeafUpArgs {
     const double2* Ainv;    // [nh][nodes_stored][q2*q2] col-major
-    const double* F;        // [NI][nF][R2]
+    const double* F;        // [R2][nF][NI]
     const double2* cF;      // [nh][nF]
     const double* D;        // p x p differentiation matrix
     double c1;              // 2/H
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(256) k_leaf_up(LeafUpArgs a) {
         const size_t g = (size_t)(leaf0 + lb) * q2 + col;
         double2 acc = make_double2(0.0, 0.0);
         for (int f = 0; f < a.nF; ++f) {
-            const double v = a.F[(g * a.nF + f) * R2 + r2];
+            const double v = a.F[((size_t)r2 * a.nF + f) * ((size_t)a.nelem * q2) + g];
             const double2 c = a.cF[(size_t)m * a.nF + f];
             acc.x += c.x * v;
             acc.y += c.y * v;
@@ -700,10 +702,11 @@ __device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, 
 }
 
 __global__ void k_recover(RecoverArgs a) {
+    // node-fastest threads: a warp reads neighbouring nodes of one E plane
     const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (tid >= a.N * a.R2) return;
-    const long long g = tid / a.R2;
-    const int r2 = (int)(tid % a.R2);
+    const long long g = tid % a.N;
+    const int r2 = (int)(tid / a.N);
     const int k = r2 >> 1, part = r2 & 1;
     double* base = a.u + (size_t)k * 3 * a.N * 2 + part;
     const double* E0 = a.E + ((size_t)0 * a.R2 + r2) * a.N;

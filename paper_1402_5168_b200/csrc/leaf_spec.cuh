@@ -42,7 +42,7 @@ struct SpecArgs {
     const double2* Dinv;    // [nh][16*16] 1/(c2 (l_i + l_j) - sigma_m), (i', j') at i'*16 + j'
     const double2* cF;      // [nh][nF]
     const double2* dE;      // [nh][nE]
-    const double* F;        // [NI][nF][R2] pole-independent RHS fields (k_pre)
+    const double* F;        // [R2][nF][NI] pole-independent RHS fields (k_pre)
     double* G;              // [nelem][R2][nF][q2] their spectral coefficients
     int q, p, nF, nE, nelem, R2, nh, ngroups, accumulate;
     double c1, c2;
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_pre(SpecArgs a) {
     for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
     for (int e = t; e < a.nF * q2; e += blockDim.x) {
         const int f = e / q2, node = e % q2;   // node = j*q + i
-        fs[f][node] = a.F[(((size_t)leaf * q2 + node) * a.nF + f) * a.R2 + r2];
+        fs[f][node] = a.F[((size_t)r2 * a.nF + f) * ((size_t)a.nelem * q2) + (size_t)leaf * q2 + node];
     }
     __syncthreads();
     // T1[f][(j, i')] = sum_i Vinv[i'][i] F_f[i][j]
