@@ -60,6 +60,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 // B gather in two phases so the global loads of chunk c+1 are in flight while
@@ -91,6 +93,18 @@ __device__ __forceinline__ void cg_fetch(const CgemmArgs& a, int m, int k, int c
         const double2 v = a.src[((size_t)m * a.src_ps + a.bi0[(size_t)node * a.K + k]) * R2 + r2];
         r.v[0] = v.x; r.v[1] = v.y;
     }
+}
+
+// modes whose B element is one gathered 16-byte value (copyable by cp.async)
+template <int MODE>
+__host__ __device__ constexpr bool cg_plain_b() { return MODE == CG_UPY || MODE == CG_DOWN || MODE == CG_LEAF_DOWN; }
+
+template <int R2T, int MODE>
+__device__ __forceinline__ const double2* cg_src_ptr(const CgemmArgs& a, int m, int k, int col) {
+    const int R2 = R2T ? R2T : a.R2;
+    const int node = col / R2, r2 = col % R2;
+    if (MODE == CG_UPY) return a.src + (size_t)m * a.src_ps * R2 + ((size_t)node * a.K + k) * R2 + r2;
+    return a.src + ((size_t)m * a.src_ps + a.bi0[(size_t)node * a.K + k]) * R2 + r2;   // DOWN, LEAF_DOWN
 }
 
 template <int MODE>
@@ -126,13 +140,16 @@ __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int
     }
 }
 
-template <int MT, int WN, int BK, int NTW = 1, int WM = 1>
+template <int MT, int WN, int BK, int NTW = 1, int WM = 1, int NST = 2>
 constexpr size_t cgemm_smem_bytes() {
-    return 2 * (size_t)BK * ((8 * MT * WM + 2) + (8 * WN * NTW + 2)) * sizeof(double2);
+    return (size_t)NST * BK * ((8 * MT * WM + 2) + (8 * WN * NTW + 2)) * sizeof(double2);
 }
 
 // MT m-tiles and NTW n-tiles per warp; WN warps side by side in n, WM in m.
-template <int MT, int WN, int BK, int R2T, int MODE, int NTW = 1, int MINB = 1, int WM = 1>
+// NST = 2: A by cp.async and B through registers, one chunk ahead.  NST >= 3
+// (plain-gather B modes): A and B both by cp.async into an NST-stage ring,
+// NST - 1 chunks in flight, one barrier per chunk.
+template <int MT, int WN, int BK, int R2T, int MODE, int NTW = 1, int MINB = 1, int WM = 1, int NST = 2>
 __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
     constexpr int BM = 8 * MT * WM, BN = 8 * WN * NTW, NT = 32 * WN * WM;
     const int R2 = R2T ? R2T : a.R2;
@@ -225,20 +242,7 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
     }
 
     const int nchunks = (a.K + BK - 1) / BK;
-    issue_A(0, 0);
-    fetch_B(0);
-    store_B(0);
-    cp_async_wait_all();
-    __syncthreads();
-    for (int ch = 0; ch < nchunks; ++ch) {
-        const int buf = ch & 1;
-        const bool more = ch + 1 < nchunks;
-        if (more) {
-            issue_A(buf ^ 1, (ch + 1) * BK);
-            fetch_B((ch + 1) * BK);
-        }
-        const double2* Ab = As(buf);
-        const double2* Bb = Bs(buf);
+    auto compute = [&](const double2* Ab, const double2* Bb) {
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
             const int kk = ks * 4 + t4;
@@ -266,11 +270,60 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
 #pragma unroll
                 for (int i = 0; i < MT; ++i) dmma884(acc[i][n][2], acc[i][n][3], av[i].y, b[n].x);    // Ci += Ai Br
         }
-        if (more) {
-            store_B(buf ^ 1);
-            cp_async_wait_all();
+    };
+    if constexpr (NST >= 3 && cg_plain_b<MODE>()) {
+        auto AsN = [&](int buf) { return sm + buf * BK * LDA; };
+        auto BsN = [&](int buf) { return sm + NST * BK * LDA + buf * BK * LDB; };
+        auto issue = [&](int buf, int k0) {
+            double2* ab = AsN(buf);
+            for (int e = tid; e < BK * BM; e += NT) {
+                const int kk = e / BM, r = e % BM;
+                const int row = row0 + r, k = k0 + kk;
+                if (row < a.rows && k < a.K) cp_async16(ab + kk * LDA + r, Am + (size_t)k * a.rows + row);
+                else ab[kk * LDA + r] = make_double2(0.0, 0.0);
+            }
+            double2* bb = BsN(buf);
+            for (int e = tid; e < BK * BN; e += NT) {
+                const int kk = e / BN, cc = e % BN;
+                const int k = k0 + kk, col = col0 + cc;
+                if (k < a.K && col < ncols) cp_async16(bb + kk * LDB + cc, cg_src_ptr<R2T, MODE>(a, m, k, col));
+                else bb[kk * LDB + cc] = make_double2(0.0, 0.0);
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int st = 0; st < NST - 1; ++st) {
+            if (st < nchunks) issue(st, st * BK);
+            else cp_async_commit();
         }
+        for (int ch = 0; ch < nchunks; ++ch) {
+            cp_async_wait_group<NST - 2>();   // chunk ch has landed (this thread's copies)
+            __syncthreads();                  // everyone's copies; the buffer refilled below is free
+            const int nx = ch + NST - 1;
+            if (nx < nchunks) issue(nx % NST, nx * BK);
+            else cp_async_commit();
+            compute(AsN(ch % NST), BsN(ch % NST));
+        }
+    } else {
+        issue_A(0, 0);
+        fetch_B(0);
+        store_B(0);
+        cp_async_wait_all();
         __syncthreads();
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int buf = ch & 1;
+            const bool more = ch + 1 < nchunks;
+            if (more) {
+                issue_A(buf ^ 1, (ch + 1) * BK);
+                fetch_B((ch + 1) * BK);
+            }
+            compute(As(buf), Bs(buf));
+            if (more) {
+                store_B(buf ^ 1);
+                cp_async_wait_all();
+            }
+            __syncthreads();
+        }
     }
     // epilogue: C[g][2 t4 + j] of each tile
 #pragma unroll

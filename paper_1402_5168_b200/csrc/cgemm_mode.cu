@@ -9,9 +9,10 @@ namespace rexp {
 namespace dev {
 namespace {
 
-template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int MINB = 1>
+template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int MINB = 1, int NST = 2>
 void cg_launch(dim3 grid, cudaStream_t s, const CgemmArgs& a) {
-    k_cgemm<MT, WN, BK, R2T, MODE, 1, MINB, WM><<<grid, 32 * WN * WM, cgemm_smem_bytes<MT, WN, BK, 1, WM>(), s>>>(a);
+    k_cgemm<MT, WN, BK, R2T, MODE, 1, MINB, WM, NST>
+        <<<grid, 32 * WN * WM, cgemm_smem_bytes<MT, WN, BK, 1, WM, NST>(), s>>>(a);
 }
 // leaf tiles: MT in {4, 5}, WN = 8; merge tiles: MT in {2, 4} with
 //   WN = 8, WM = 1 | WN = 4, WM = 2 | WN = 2, WM = 4
@@ -27,7 +28,25 @@ void cg_tiles_b(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
         else cg_launch<4, 8, BK, R2T, MODE, 1, MINB>(grid, s, a);
     }
 }
-// MINB = 4: register budget for 4 resident 256-thread CTAs per SM (<= 64 registers)
+// 3-stage cp.async ring (plain-gather B modes), MINB = 1
+template <int BK, int R2T, int MODE>
+void cg_tiles_s3(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    if constexpr (MODE == CG_UPY || MODE == CG_DOWN) {
+        if (MT == 2) {
+            if (WN == 2) cg_launch<2, 2, BK, R2T, MODE, 4, 1, 3>(grid, s, a);
+            else if (WN == 4) cg_launch<2, 4, BK, R2T, MODE, 2, 1, 3>(grid, s, a);
+            else cg_launch<2, 8, BK, R2T, MODE, 1, 1, 3>(grid, s, a);
+        } else {
+            if (WN == 2) cg_launch<4, 2, BK, R2T, MODE, 4, 1, 3>(grid, s, a);
+            else if (WN == 4) cg_launch<4, 4, BK, R2T, MODE, 2, 1, 3>(grid, s, a);
+            else cg_launch<4, 8, BK, R2T, MODE, 1, 1, 3>(grid, s, a);
+        }
+    } else {
+        cg_tiles_b<BK, R2T, MODE, 1>(MT, WN, grid, s, a);
+    }
+}
+// MINB = 4: register budget for 4 resident 256-thread CTAs per SM (<= 64 registers);
+// MINB = 3 selects the 3-stage cp.async pipeline instead (StageCfg::minb)
 template <int BK, int R2T, int MODE>
 void cg_tiles(int MT, int WN, int MINB, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     if (MODE == CG_LEAF_UP || MODE == CG_LEAF_DOWN) {
@@ -36,12 +55,13 @@ void cg_tiles(int MT, int WN, int MINB, dim3 grid, cudaStream_t s, const CgemmAr
         return;
     }
     if (MINB >= 4) cg_tiles_b<BK, R2T, MODE, 4>(MT, WN, grid, s, a);
+    else if (MINB == 3) cg_tiles_s3<BK, R2T, MODE>(MT, WN, grid, s, a);
     else cg_tiles_b<BK, R2T, MODE, 1>(MT, WN, grid, s, a);
 }
-template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int MINB = 1>
+template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int MINB = 1, int NST = 2>
 void cg_allow1() {
-    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2T, MODE, 1, MINB, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+    cudaFuncSetAttribute(k_cgemm<MT, WN, BK, R2T, MODE, 1, MINB, WM, NST>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 template <int BK, int R2T, int MODE>
 void cg_allow_tiles() {
@@ -53,6 +73,11 @@ void cg_allow_tiles() {
     cg_allow1<4, 2, BK, R2T, MODE, 4>(); cg_allow1<4, 4, BK, R2T, MODE, 2>(); cg_allow1<4, 8, BK, R2T, MODE>();
     cg_allow1<2, 2, BK, R2T, MODE, 4, 4>(); cg_allow1<2, 4, BK, R2T, MODE, 2, 4>(); cg_allow1<2, 8, BK, R2T, MODE, 1, 4>();
     cg_allow1<4, 2, BK, R2T, MODE, 4, 4>(); cg_allow1<4, 4, BK, R2T, MODE, 2, 4>(); cg_allow1<4, 8, BK, R2T, MODE, 1, 4>();
+    if constexpr (MODE == CG_UPY || MODE == CG_DOWN) {
+        cg_allow1<2, 2, BK, R2T, MODE, 4, 1, 3>(); cg_allow1<2, 4, BK, R2T, MODE, 2, 1, 3>();
+        cg_allow1<2, 8, BK, R2T, MODE, 1, 1, 3>(); cg_allow1<4, 2, BK, R2T, MODE, 4, 1, 3>();
+        cg_allow1<4, 4, BK, R2T, MODE, 2, 1, 3>(); cg_allow1<4, 8, BK, R2T, MODE, 1, 1, 3>();
+    }
 }
 
 // BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16;

@@ -1390,6 +1390,18 @@ int DeviceStore::tune_stages(bool measure) {
     t_root = StageCfg();
     t_root.kind = (shared && (R2 > 2 || !gemv_ok)) ? 0 : 1;
     cg_tile(ns, R2, t_root.MT, t_root.WN);
+    {
+        // test hook: REXP_GEMM_STAGES=3 forces the 3-stage cp.async GEMM on every
+        // UP-Y / DOWN stage that runs as a GEMM (no autotuning)
+        const char* st = std::getenv("REXP_GEMM_STAGES");
+        if (st && std::string(st) == "3") {
+            for (size_t li = 0; li < nl; ++li) {
+                if (t_upy[li].kind == 0) t_upy[li].minb = 3;
+                if (t_down[li].kind == 0) t_down[li].minb = 3;
+            }
+            return REXP_OK;
+        }
+    }
     const char* env = std::getenv("REXP_AUTOTUNE");
     if (!measure || (env && std::string(env) == "0") || !shared) return REXP_OK;
 
@@ -1426,13 +1438,16 @@ int DeviceStore::tune_stages(bool measure) {
     };
     auto tune = [&](int kind, size_t li, StageCfg& best) {
         std::vector<StageCfg> cands;
-        for (int minb : {1, 4})
+        // minb: 1 = default, 4 = register-capped, 3 = 3-stage cp.async ring (UP-Y / DOWN)
+        for (int minb : {1, 4, 3}) {
+            if (minb == 3 && kind != 1 && kind != 2) continue;
             for (int mt : {2, 4})
                 for (int wn : {2, 4, 8}) {
                     StageCfg c;
                     c.kind = 0; c.MT = mt; c.WN = wn; c.minb = minb;
                     cands.push_back(c);
                 }
+        }
         if (gemv_ok) {
             for (int rb : {32, 64, 128, 256}) {
                 StageCfg c;
@@ -1465,7 +1480,7 @@ std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
         return c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
-                                 (c.minb > 1 ? "r" : "");
+                                 (c.minb == 4 ? "r" : c.minb == 3 ? "s3" : "");
     };
     std::string s = tuned ? "tuned:" : "default:";
     for (size_t li = 0; li < levels.size(); ++li)

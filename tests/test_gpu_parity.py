@@ -134,6 +134,24 @@ def test_config0_lanes_chunks_graph(c0, lanes, chunk, graph, monkeypatch):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_config0_three_stage_gemm(c0, nrhs, monkeypatch):
+    """The 3-stage cp.async merge GEMM (an autotuner candidate) forced on every
+    GEMM stage of the up-Y and down sweeps (REXP_GEMM_STAGES=3), compile-time
+    and runtime R2."""
+    cfg, m, op, u0 = c0
+    Lam = cfg["Lambda_tau"] / cfg["tau"]
+    monkeypatch.setenv("REXP_GEMM_STAGES", "3")
+    U = np.stack([rsw_initial_state(m.x, m.y, cfg["seed"] + 10 * k) for k in range(nrhs)])
+    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], nrhs=nrhs)
+    assert "s3" in h.stage_report
+    got = _gpu_apply(h, U, 2)
+    errs = [rel_l2(got[k], op.evolve(U[k], 2)) for k in range(nrhs)]
+    print(f"3-stage GEMM nrhs {nrhs}: max rel L2 {max(errs):.3e}")
+    assert max(errs) <= TOL
+    h.close()
+
+
 def test_edge_cases_zero_state_and_zero_steps(c0):
     cfg, m, op, u0 = c0
     Lam = cfg["Lambda_tau"] / cfg["tau"]
