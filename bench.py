@@ -137,15 +137,19 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
     q2, e = q * q, n * n
     lv = tree_dims(n, q)
     per = lambda nodes: 1 if shared else nodes
+    # the cylinder level of the shared store is applied as the symmetric half
+    # pair (A11 +- A12): half the operator bytes and half the flops
+    sym = shared and R2 in (2, 4, 8)
+    lv = [(nd, n3, nx, 0.5 if (sym and i == len(lv) - 1) else 1.0) for i, (nd, n3, nx) in enumerate(lv)]
     merge = {
-        "merge_up": (sum(nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx in lv),
-                     sum(nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx in lv)),
+        "merge_up": (sum(hf * nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx, hf in lv),
+                     sum(hf * nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx, hf in lv)),
         # shared store: Fourier root (two DFTs over the n elements of the 2nq seam
         # unknowns, n blocks of (2q)^2); per-node: dense (2nq)^2
         "root": ((nh * R2 * (2 * 2 * n * q * n * 8 + n * (2 * q) ** 2 * 8), nh * n * (2 * q) ** 2 * 16) if shared
                  else (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16)),
-        "merge_down": (sum(nh * nd * n3 * nx * R2 * 8 for nd, n3, nx in lv),
-                       sum(nh * per(nd) * n3 * nx * 16 for nd, n3, nx in lv)),
+        "merge_down": (sum(hf * nh * nd * n3 * nx * R2 * 8 for nd, n3, nx, hf in lv),
+                       sum(hf * nh * per(nd) * n3 * nx * 16 for nd, n3, nx, hf in lv)),
     }
     if leaf == "spectral":
         unit = nh * e * R2

@@ -413,6 +413,153 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
 }
 
 // --------------------------------------------------------------------------
+// k_gemv_sym: the cylinder level of the shared store.  The shift x -> x + n/2
+// maps the cylinder onto itself, exchanging its children a, b, the two
+// vertical seams (mid, wrap) and each a-side boundary segment with its b-side
+// partner; with Ta = Tb every operator of the level is [[A11, A12], [A12, A11]]
+// in those blocks (pinned by tests/test_setup_host.py), so it is stored as the
+// half-size pair M+ = A11 + A12, M- = A11 - A12 ([M+ | M-], column-major) and
+// applied in sum / difference coordinates:
+//   x+ = x_A + x_B, x- = x_A - x_B,  y_A = (M+ x+ + M- x-)/2,  y_B = (M+ x+ - M- x-)/2.
+// Pairings: interface t <-> t + n3/2; boundary (ext) row r of a.bottom / a.top
+// <-> the same row of b.bottom / b.top (ext order [a.bot, b.bot, a.top, b.top]).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ int sym_ext_a(int c, int acq) { return c < acq ? c : acq + c; }
+
+template <int R2, int NB, int MODE>
+__global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a) {
+    extern __shared__ double2 sm[];
+    const int m = blockIdx.y;
+    const int grp = blockIdx.x / a.nrowblk;
+    const int rb = blockIdx.x % a.nrowblk;
+    const int node0 = grp * NB;
+    const int hc = a.cols, hr = a.rows;                 // half sizes
+    const int n3 = MODE == MODE_DOWN ? 2 * hr : 2 * (MODE == MODE_UPX ? hr : hc);
+    const int next = MODE == MODE_DOWN ? 2 * hc : 2 * hr;   // UPX: unused
+    const int acq = next / 4;
+    double2* xs = sm;                                   // [NB][2][hc][R2]: x+, x-
+    double2* red = sm + (size_t)NB * 2 * hc * R2;       // [CS][RB][2*NB*R2]
+    const double2* src = a.xsrc + (size_t)m * a.xsrc_ps * R2;
+    for (int t = threadIdx.x; t < NB * hc * R2; t += blockDim.x) {
+        const int r2 = t % R2;
+        const int c = (t / R2) % hc;
+        const int nb = t / (R2 * hc);
+        const int node = node0 + nb;
+        double2 xa, xb;
+        if (MODE == MODE_UPX) {           // s3 = h^a_3 + h^b_3 at interface t = c (mid), c + n3/2 (wrap)
+            const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
+            const double2 a0 = src[(size_t)(base + a.xi0[c]) * R2 + r2], a1 = src[(size_t)(base + a.xi1[c]) * R2 + r2];
+            const double2 b0 = src[(size_t)(base + a.xi0[c + hc]) * R2 + r2];
+            const double2 b1 = src[(size_t)(base + a.xi1[c + hc]) * R2 + r2];
+            xa = make_double2(a0.x + a1.x, a0.y + a1.y);
+            xb = make_double2(b0.x + b1.x, b0.y + b1.y);
+        } else if (MODE == MODE_UPY) {    // w3, contiguous
+            xa = src[((size_t)node * n3 + c) * R2 + r2];
+            xb = src[((size_t)node * n3 + c + hc) * R2 + r2];
+        } else {                          // DOWN: u_ext gathered at the paired boundary rows
+            const int ca = sym_ext_a(c, acq);
+            xa = src[(size_t)a.xi0[(size_t)node * next + ca] * R2 + r2];
+            xb = src[(size_t)a.xi0[(size_t)node * next + ca + acq] * R2 + r2];
+        }
+        xs[((nb * 2 + 0) * hc + c) * R2 + r2] = make_double2(xa.x + xb.x, xa.y + xb.y);
+        xs[((nb * 2 + 1) * hc + c) * R2 + r2] = make_double2(xa.x - xb.x, xa.y - xb.y);
+    }
+    __syncthreads();
+    const int rl = threadIdx.x % a.RB;
+    const int cs = threadIdx.x / a.RB;
+    const int row = rb * a.RB + rl;
+    double2 ap[NB][R2], am[NB][R2];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int r = 0; r < R2; ++r) ap[nb][r] = am[nb][r] = make_double2(0.0, 0.0);
+    if (row < hr && cs < a.CS) {
+        const double2* Mp = a.M + (size_t)m * 2 * hr * hc + row;
+        const double2* Mm = Mp + (size_t)hr * hc;
+        const int CS = a.CS;
+        int c = cs;
+        for (; c + 3 * CS < hc; c += 4 * CS) {
+            double2 vp[4], vm[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                vp[u] = ldg2(Mp + (size_t)(c + u * CS) * hr);
+                vm[u] = ldg2(Mm + (size_t)(c + u * CS) * hr);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int r = 0; r < R2; ++r) {
+                        cfma(ap[nb][r], vp[u], xs[((nb * 2 + 0) * hc + c + u * CS) * R2 + r]);
+                        cfma(am[nb][r], vm[u], xs[((nb * 2 + 1) * hc + c + u * CS) * R2 + r]);
+                    }
+        }
+        for (; c < hc; c += CS) {
+            const double2 vp = ldg2(Mp + (size_t)c * hr), vm = ldg2(Mm + (size_t)c * hr);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                for (int r = 0; r < R2; ++r) {
+                    cfma(ap[nb][r], vp, xs[((nb * 2 + 0) * hc + c) * R2 + r]);
+                    cfma(am[nb][r], vm, xs[((nb * 2 + 1) * hc + c) * R2 + r]);
+                }
+        }
+    }
+    if (a.CS > 1) {
+        if (cs < a.CS) {
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                for (int r = 0; r < R2; ++r) {
+                    red[((size_t)cs * a.RB + rl) * (2 * NB * R2) + nb * R2 + r] = ap[nb][r];
+                    red[((size_t)cs * a.RB + rl) * (2 * NB * R2) + (NB + nb) * R2 + r] = am[nb][r];
+                }
+        }
+        __syncthreads();
+        if (cs == 0) {
+            for (int s = 1; s < a.CS; ++s)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int r = 0; r < R2; ++r) {
+                        const double2 vp = red[((size_t)s * a.RB + rl) * (2 * NB * R2) + nb * R2 + r];
+                        const double2 vm = red[((size_t)s * a.RB + rl) * (2 * NB * R2) + (NB + nb) * R2 + r];
+                        ap[nb][r].x += vp.x; ap[nb][r].y += vp.y;
+                        am[nb][r].x += vm.x; am[nb][r].y += vm.y;
+                    }
+        }
+    }
+    if (cs != 0 || row >= hr) return;
+    double2* dst = a.ydst + (size_t)m * a.ydst_ps * R2;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        const int node = node0 + nb;
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+            const double2 yA = make_double2(0.5 * (ap[nb][r].x + am[nb][r].x), 0.5 * (ap[nb][r].y + am[nb][r].y));
+            const double2 yB = make_double2(0.5 * (ap[nb][r].x - am[nb][r].x), 0.5 * (ap[nb][r].y - am[nb][r].y));
+            if (MODE == MODE_UPX) {
+                dst[((size_t)node * n3 + row) * R2 + r] = yA;
+                dst[((size_t)node * n3 + row + hr) * R2 + r] = yB;
+            } else if (MODE == MODE_UPY) {
+                const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
+                const int ra = sym_ext_a(row, acq), rbw = ra + acq;
+                const double2* add = a.ysrc + (size_t)m * a.ysrc_ps * R2;
+                const double2 ea = add[(size_t)(base + a.yi[ra]) * R2 + r], eb = add[(size_t)(base + a.yi[rbw]) * R2 + r];
+                dst[((size_t)node * next + ra) * R2 + r] = make_double2(yA.x + ea.x, yA.y + ea.y);
+                dst[((size_t)node * next + rbw) * R2 + r] = make_double2(yB.x + eb.x, yB.y + eb.y);
+            } else {
+                const double2* w3 = a.ysrc + (size_t)m * a.ysrc_ps * R2;
+                const double2 wa = w3[((size_t)node * n3 + row) * R2 + r], wb = w3[((size_t)node * n3 + row + hr) * R2 + r];
+                dst[(size_t)a.yo[(size_t)node * n3 + row] * R2 + r] = make_double2(yA.x + wa.x, yA.y + wa.y);
+                dst[(size_t)a.yo[(size_t)node * n3 + row + hr] * R2 + r] = make_double2(yB.x + wb.x, yB.y + wb.y);
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
 // k_root_fourier: periodic closure of the shared store in Fourier space.
 // The seam operator is block circulant in the element index e along x
 // (setup_host.cpp): s = X (h^a_3 + h^b_3) is applied as
@@ -1007,9 +1154,13 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         D.nodes = L.nodes; D.n3 = L.n3; D.next = L.next; D.nchild = L.nchild; D.child_nodes = L.child_nodes;
         D.nbx = L.nbx; D.dir = L.dir;
         const size_t st = shared ? 1 : static_cast<size_t>(L.nodes);
-        D.ppX = st * L.n3 * L.n3;
-        D.ppY = st * L.next * L.n3;
-        D.ppS = st * L.n3 * L.next;
+        // the cylinder level of the shared store keeps only the symmetric half pair
+        // [M+ | M-] of each operator (k_gemv_sym; GEMV-compatible R2 only)
+        D.sym = shared && (R2 == 2 || R2 == 4 || R2 == 8) && li + 1 == T.levels.size() && L.nodes == 2 &&
+                L.next == 2 * T.n * T.q && L.n3 % 2 == 0 && std::getenv("REXP_NO_SYM") == nullptr;
+        D.ppX = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * (L.n3 / 2) : st * L.n3 * L.n3;
+        D.ppY = D.sym ? 2 * static_cast<size_t>(L.next / 2) * (L.n3 / 2) : st * L.next * L.n3;
+        D.ppS = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * (L.next / 2) : st * L.n3 * L.next;
         if ((rc = alloc(&D.X, nh * D.ppX))) return rc;
         if ((rc = alloc(&D.Y, nh * D.ppY))) return rc;
         if ((rc = alloc(&D.S, nh * D.ppS))) return rc;
@@ -1127,6 +1278,46 @@ int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
     }
     for (size_t li = 0; li < levels.size(); ++li) {
         Level& D = levels[li];
+        if (D.sym) {
+            // [M+ | M-] per pole from the full (column-major) X, Y, S
+            const int n3 = D.n3, ne = D.next, h3 = n3 / 2, hx = ne / 2, acq = ne / 4;
+            auto ext_a = [acq](int c) { return c < acq ? c : acq + c; };
+            const HostLevelOps& H = ops[li + 1];
+            const size_t npole = H.m[0].size() / (static_cast<size_t>(n3) * n3);
+            std::vector<cd> X2(npole * D.ppX), Y2(npole * D.ppY), S2(npole * D.ppS);
+            for (size_t pl = 0; pl < npole; ++pl) {
+                const cd* X = H.m[0].data() + pl * n3 * n3;
+                const cd* Y = H.m[1].data() + pl * static_cast<size_t>(ne) * n3;
+                const cd* S = H.m[2].data() + pl * static_cast<size_t>(n3) * ne;
+                cd* xo = X2.data() + pl * D.ppX;
+                cd* yo = Y2.data() + pl * D.ppY;
+                cd* so = S2.data() + pl * D.ppS;
+                for (int c = 0; c < h3; ++c)        // X: rows mid, cols (mid, wrap)
+                    for (int r = 0; r < h3; ++r) {
+                        const cd a11 = X[static_cast<size_t>(c) * n3 + r], a12 = X[static_cast<size_t>(c + h3) * n3 + r];
+                        xo[static_cast<size_t>(c) * h3 + r] = a11 + a12;
+                        xo[static_cast<size_t>(h3) * h3 + static_cast<size_t>(c) * h3 + r] = a11 - a12;
+                    }
+                for (int c = 0; c < h3; ++c)        // Y: rows a-side ext, cols (mid, wrap)
+                    for (int r = 0; r < hx; ++r) {
+                        const int ra = ext_a(r);
+                        const cd a11 = Y[static_cast<size_t>(c) * ne + ra], a12 = Y[static_cast<size_t>(c + h3) * ne + ra];
+                        yo[static_cast<size_t>(c) * hx + r] = a11 + a12;
+                        yo[static_cast<size_t>(hx) * h3 + static_cast<size_t>(c) * hx + r] = a11 - a12;
+                    }
+                for (int c = 0; c < hx; ++c)        // S: rows mid, cols (a-side, b-side) ext
+                    for (int r = 0; r < h3; ++r) {
+                        const int ca = ext_a(c);
+                        const cd a11 = S[static_cast<size_t>(ca) * n3 + r], a12 = S[static_cast<size_t>(ca + acq) * n3 + r];
+                        so[static_cast<size_t>(c) * h3 + r] = a11 + a12;
+                        so[static_cast<size_t>(h3) * hx + static_cast<size_t>(c) * h3 + r] = a11 - a12;
+                    }
+            }
+            if ((rc = up(X2, D.X, D.ppX))) return rc;
+            if ((rc = up(Y2, D.Y, D.ppY))) return rc;
+            if ((rc = up(S2, D.S, D.ppS))) return rc;
+            continue;
+        }
         if ((rc = up(ops[li + 1].m[0], D.X, D.ppX))) return rc;
         if ((rc = up(ops[li + 1].m[1], D.Y, D.ppY))) return rc;
         if ((rc = up(ops[li + 1].m[2], D.S, D.ppS))) return rc;
@@ -1189,10 +1380,26 @@ void allow_all_nb() {
 }
 template <int R2>
 void allow_all() {
+    allow_smem(k_gemv_sym<R2, 1, MODE_UPX>); allow_smem(k_gemv_sym<R2, 1, MODE_UPY>); allow_smem(k_gemv_sym<R2, 1, MODE_DOWN>);
+    allow_smem(k_gemv_sym<R2, 2, MODE_UPX>); allow_smem(k_gemv_sym<R2, 2, MODE_UPY>); allow_smem(k_gemv_sym<R2, 2, MODE_DOWN>);
     allow_all_nb<R2, 1>();
     allow_all_nb<R2, 2>();
     allow_all_nb<R2, 4>();
     allow_all_nb<R2, 8>();
+}
+
+template <int MODE>
+void launch_gemv_sym(int R2, int NB, dim3 grid, size_t smem, cudaStream_t s, const GemvArgs& a) {
+    if (R2 == 2) {
+        if (NB == 2) k_gemv_sym<2, 2, MODE><<<grid, 256, smem, s>>>(a);
+        else k_gemv_sym<2, 1, MODE><<<grid, 256, smem, s>>>(a);
+    } else if (R2 == 4) {
+        if (NB == 2) k_gemv_sym<4, 2, MODE><<<grid, 256, smem, s>>>(a);
+        else k_gemv_sym<4, 1, MODE><<<grid, 256, smem, s>>>(a);
+    } else {
+        if (NB == 2) k_gemv_sym<8, 2, MODE><<<grid, 256, smem, s>>>(a);
+        else k_gemv_sym<8, 1, MODE><<<grid, 256, smem, s>>>(a);
+    }
 }
 
 GemvArgs gemv_shape(int rows, int cols, int nodes, bool shared, int rbmax = 64) {
@@ -1309,6 +1516,36 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     const double2* hc = d_h[li % 2];
     double2* hp = d_h[(li + 1) % 2];
     const int cls = kind == 2 ? T_MERGE_DOWN : T_MERGE_UP;
+    if (L.sym) {
+        const int NB = pick_nb(L.nodes, R2, shared) >= 2 ? 2 : 1;
+        const int h3 = L.n3 / 2, hx = L.next / 2;
+        GemvArgs g;
+        if (kind == 0) {
+            g = gemv_shape(h3, h3, L.nodes, true, cfg.rb);
+            g.M = L.X + static_cast<size_t>(m0) * L.ppX; g.xsrc = hc; g.xsrc_ps = hstride; g.xi0 = L.ia3; g.xi1 = L.ib3;
+            g.ydst = L.w3; g.ydst_ps = static_cast<long long>(L.nodes) * L.n3;
+        } else if (kind == 1) {
+            g = gemv_shape(hx, h3, L.nodes, true, cfg.rb);
+            g.M = L.Y + static_cast<size_t>(m0) * L.ppY; g.xsrc = L.w3; g.xsrc_ps = static_cast<long long>(L.nodes) * L.n3;
+            g.ysrc = hc; g.ysrc_ps = hstride; g.yi = L.ext;
+            g.ydst = hp; g.ydst_ps = hstride;
+        } else {
+            g = gemv_shape(h3, hx, L.nodes, true, cfg.rb);
+            g.M = L.S + static_cast<size_t>(m0) * L.ppS; g.xsrc = d_edge; g.xsrc_ps = NE; g.xi0 = L.gext;
+            g.ysrc = L.w3; g.ysrc_ps = static_cast<long long>(L.nodes) * L.n3;
+            g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
+        }
+        g.nbx = L.nbx; g.xdir = L.dir == 0 ? 1 : 0; g.nchild = L.nchild;
+        const dim3 grid((L.nodes / NB) * g.nrowblk, pc);
+        const size_t smem = (static_cast<size_t>(NB) * 2 * g.cols * R2 +
+                             static_cast<size_t>(g.CS > 1 ? g.CS : 0) * g.RB * 2 * NB * R2) * sizeof(double2);
+        tbeg(s);
+        if (kind == 0) launch_gemv_sym<MODE_UPX>(R2, NB, grid, smem, s, g);
+        else if (kind == 1) launch_gemv_sym<MODE_UPY>(R2, NB, grid, smem, s, g);
+        else launch_gemv_sym<MODE_DOWN>(R2, NB, grid, smem, s, g);
+        tend(cls, s);
+        return REXP_OK;
+    }
     if (cfg.kind == 0) {
         CgemmArgs a{};
         a.nodes = L.nodes; a.R2 = R2;
@@ -1380,7 +1617,7 @@ int DeviceStore::tune_stages(bool measure) {
         const Level& L = levels[li];
         const bool use_gemm = shared && (L.nodes * R2 >= 4 || !gemv_ok);
         StageCfg c;
-        c.kind = use_gemm ? 0 : 1;
+        c.kind = L.sym ? 2 : use_gemm ? 0 : 1;
         cg_tile(L.n3, L.nodes * R2, c.MT, c.WN);
         t_upx[li] = c;
         t_down[li] = c;
@@ -1438,6 +1675,19 @@ int DeviceStore::tune_stages(bool measure) {
     };
     auto tune = [&](int kind, size_t li, StageCfg& best) {
         std::vector<StageCfg> cands;
+        if (kind != 3 && levels[li].sym) {
+            for (int rb : {32, 64, 128, 256}) {
+                StageCfg c;
+                c.kind = 2; c.rb = rb;
+                cands.push_back(c);
+            }
+            float bt = time_cfg(kind, li, best);
+            for (const StageCfg& c : cands) {
+                const float t = time_cfg(kind, li, c);
+                if (t < bt) { bt = t; best = c; }
+            }
+            return;
+        }
         // minb: 1 = default, 4 = register-capped, 3 = 3-stage cp.async ring (UP-Y / DOWN)
         for (int minb : {1, 4, 3}) {
             if (minb == 3 && kind != 1 && kind != 2) continue;
@@ -1478,7 +1728,7 @@ int DeviceStore::tune_stages(bool measure) {
 
 std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
-        return c.kind == 1 ? "gemv" + std::to_string(c.rb)
+        return c.kind == 2 ? "sym" + std::to_string(c.rb) : c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
                                  (c.minb == 4 ? "r" : c.minb == 3 ? "s3" : "");
     };

@@ -12,7 +12,7 @@ namespace rexp {
 namespace dev {
 
 struct StageCfg {
-    int kind = 0;   // 0: DMMA GEMM (k_cgemm), 1: GEMV (k_gemv)
+    int kind = 0;   // 0: DMMA GEMM (k_cgemm), 1: GEMV (k_gemv), 2: symmetric-pair GEMV (k_gemv_sym)
     int MT = 4, WN = 8;
     int minb = 1;   // 4: register-capped variant (4 resident CTAs per SM)
     int rb = 64;    // GEMV row block (CS = 256 / rb column groups)
@@ -20,6 +20,7 @@ struct StageCfg {
 
 struct Level {
     int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0, nbx = 1, dir = 0;
+    bool sym = false;   // cylinder level stored as the symmetric half pair [M+ | M-] (k_gemv_sym)
     double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
     int *ia3 = nullptr, *ib3 = nullptr, *ext = nullptr, *gext = nullptr, *g3 = nullptr;
     double2* w3 = nullptr;                              // [chunk][nodes][n3][R2]

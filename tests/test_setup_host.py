@@ -262,3 +262,32 @@ def test_merge_gather_indices_affine_in_node(n):
         for which, cnt in ((0, n3), (1, n3), (2, ne)):
             idx = api.export_index(h, lev, which, nodes * cnt).reshape(nodes, cnt)
             assert (ca[:, None] * nc + idx[0][None, :] == idx).all()
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_cylinder_level_swap_symmetry(n):
+    """DESIGN.md §2 "cylinder symmetry": with constant coefficients the shift
+    x -> x + n/2 maps the cylinder onto itself, exchanging its children a, b,
+    the mid / wrap seams (interface t <-> t + n3/2) and each a-side boundary row
+    with its b-side partner (ext order [a.bot, b.bot, a.top, b.top]).  The
+    cylinder-level X, Y, S are therefore [[A11, A12], [A12, A11]] in those
+    blocks, which the device store exploits (half-size pair A11 +- A12)."""
+    from paper_1402_5168_b200 import api
+    h = api.setup("rsw", n=n, p=6, tau=0.2, delta=1e-10, Lambda=100.0, f=1.0, device=-1, store="shared")
+    lev = api.export_num_levels(h) - 2
+    nodes, _, n3, ne, _ = api.export_level_info(h, lev)[:5]
+    assert nodes == 2 and ne == 2 * n * 4
+    h3, acq = n3 // 2, ne // 4
+    rA = np.r_[np.arange(acq), 2 * acq + np.arange(acq)]
+    rB = rA + acq
+    for half in (0, h.num_half_poles - 1):
+        X = api.export_matrix(h, half, lev, 0, 0, n3, n3)
+        Y = api.export_matrix(h, half, lev, 0, 1, ne, n3)
+        S = api.export_matrix(h, half, lev, 0, 2, n3, ne)
+        tol = 1e-13
+        assert np.abs(X[:h3, :h3] - X[h3:, h3:]).max() <= tol * np.abs(X).max()
+        assert np.abs(X[:h3, h3:] - X[h3:, :h3]).max() <= tol * np.abs(X).max()
+        assert np.abs(Y[rA][:, :h3] - Y[rB][:, h3:]).max() <= tol * np.abs(Y).max()
+        assert np.abs(Y[rA][:, h3:] - Y[rB][:, :h3]).max() <= tol * np.abs(Y).max()
+        assert np.abs(S[:h3][:, rA] - S[h3:][:, rB]).max() <= tol * np.abs(S).max()
+        assert np.abs(S[:h3][:, rB] - S[h3:][:, rA]).max() <= tol * np.abs(S).max()
