@@ -478,22 +478,42 @@ __global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a) {
         const double2* Mm = Mp + (size_t)hr * hc;
         const int CS = a.CS;
         int c = cs;
-        for (; c + 3 * CS < hc; c += 4 * CS) {
-            double2 vp[4], vm[4];
+        // software pipelined: the next 4 columns of both matrices (8 loads) are in
+        // flight while the current 4 are used
+        if (c + 3 * CS < hc) {
+            double2 vp[4], vm[4], np[4], nm[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 vp[u] = ldg2(Mp + (size_t)(c + u * CS) * hr);
                 vm[u] = ldg2(Mm + (size_t)(c + u * CS) * hr);
             }
+            for (;;) {
+                const int cn = c + 4 * CS;
+                const bool more = cn + 3 * CS < hc;
+                if (more) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                    for (int r = 0; r < R2; ++r) {
-                        cfma(ap[nb][r], vp[u], xs[((nb * 2 + 0) * hc + c + u * CS) * R2 + r]);
-                        cfma(am[nb][r], vm[u], xs[((nb * 2 + 1) * hc + c + u * CS) * R2 + r]);
+                    for (int u = 0; u < 4; ++u) {
+                        np[u] = ldg2(Mp + (size_t)(cn + u * CS) * hr);
+                        nm[u] = ldg2(Mm + (size_t)(cn + u * CS) * hr);
                     }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                        for (int r = 0; r < R2; ++r) {
+                            cfma(ap[nb][r], vp[u], xs[((nb * 2 + 0) * hc + c + u * CS) * R2 + r]);
+                            cfma(am[nb][r], vm[u], xs[((nb * 2 + 1) * hc + c + u * CS) * R2 + r]);
+                        }
+                c = cn;
+                if (!more) break;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    vp[u] = np[u];
+                    vm[u] = nm[u];
+                }
+            }
         }
         for (; c < hc; c += CS) {
             const double2 vp = ldg2(Mp + (size_t)c * hr), vm = ldg2(Mm + (size_t)c * hr);
