@@ -413,30 +413,36 @@ __global__ void __launch_bounds__(256) k_gemv(GemvArgs a) {
 }
 
 // --------------------------------------------------------------------------
-// k_gemv_sym: the cylinder level of the shared store.  The shift x -> x + n/2
-// maps the cylinder onto itself, exchanging its children a, b, the two
-// vertical seams (mid, wrap) and each a-side boundary segment with its b-side
-// partner; with Ta = Tb every operator of the level is [[A11, A12], [A12, A11]]
-// in those blocks (pinned by tests/test_setup_host.py), so it is stored as the
-// half-size pair M+ = A11 + A12, M- = A11 - A12 ([M+ | M-], column-major) and
-// applied in sum / difference coordinates:
-//   x+ = x_A + x_B, x- = x_A - x_B,  y_A = (M+ x+ + M- x-)/2,  y_B = (M+ x+ - M- x-)/2.
-// Pairings: interface t <-> t + n3/2; boundary (ext) row r of a.bottom / a.top
-// <-> the same row of b.bottom / b.top (ext order [a.bot, b.bot, a.top, b.top]).
+// k_gemv_sym: top merge levels of the shared store applied in symmetric-pair
+// form.  A geometric symmetry of the level (the reflection along its
+// interface, which maps each child box onto itself) acts on the edge data of
+// the spectral edge basis as a signed involution P without fixed points:
+// position A <-> B with sign s (s = eigenvector parity for segments it
+// reverses, +1 otherwise).  Every operator of the level commutes with P, so it
+// is stored as the half-size pair M+- = A_AA +- A_AB S ([M+ | M-], column-major)
+// and applied as
+//   x+- = x_A +- s x_B,  y_A = (M+ x+ + M- x-)/2,  y_B = s (M+ x+ - M- x-)/2
+// (pinned in the nodal basis by tests/test_setup_host.py).  GemvArgs.rows /
+// .cols are the half sizes; the pairs of the input and output index spaces come
+// from SymPairs.
 // --------------------------------------------------------------------------
-__device__ __forceinline__ int sym_ext_a(int c, int acq) { return c < acq ? c : acq + c; }
+struct SymPairs {
+    const int *iA, *iB;     // input pairs (A, B), sign is
+    const double* is;
+    const int *oA, *oB;     // output pairs
+    const double* os;
+    int n3, next;
+};
 
 template <int R2, int NB, int MODE>
-__global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a) {
+__global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a, SymPairs sp) {
     extern __shared__ double2 sm[];
     const int m = blockIdx.y;
     const int grp = blockIdx.x / a.nrowblk;
     const int rb = blockIdx.x % a.nrowblk;
     const int node0 = grp * NB;
     const int hc = a.cols, hr = a.rows;                 // half sizes
-    const int n3 = MODE == MODE_DOWN ? 2 * hr : 2 * (MODE == MODE_UPX ? hr : hc);
-    const int next = MODE == MODE_DOWN ? 2 * hc : 2 * hr;   // UPX: unused
-    const int acq = next / 4;
+    const int n3 = sp.n3, next = sp.next;
     double2* xs = sm;                                   // [NB][2][hc][R2]: x+, x-
     double2* red = sm + (size_t)NB * 2 * hc * R2;       // [CS][RB][2*NB*R2]
     const double2* src = a.xsrc + (size_t)m * a.xsrc_ps * R2;
@@ -445,24 +451,24 @@ __global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a) {
         const int c = (t / R2) % hc;
         const int nb = t / (R2 * hc);
         const int node = node0 + nb;
+        const int pa = sp.iA[c], pb = sp.iB[c];
         double2 xa, xb;
-        if (MODE == MODE_UPX) {           // s3 = h^a_3 + h^b_3 at interface t = c (mid), c + n3/2 (wrap)
+        if (MODE == MODE_UPX) {           // s3 = h^a_3 + h^b_3 at interface positions pa, pb
             const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
-            const double2 a0 = src[(size_t)(base + a.xi0[c]) * R2 + r2], a1 = src[(size_t)(base + a.xi1[c]) * R2 + r2];
-            const double2 b0 = src[(size_t)(base + a.xi0[c + hc]) * R2 + r2];
-            const double2 b1 = src[(size_t)(base + a.xi1[c + hc]) * R2 + r2];
+            const double2 a0 = src[(size_t)(base + a.xi0[pa]) * R2 + r2], a1 = src[(size_t)(base + a.xi1[pa]) * R2 + r2];
+            const double2 b0 = src[(size_t)(base + a.xi0[pb]) * R2 + r2], b1 = src[(size_t)(base + a.xi1[pb]) * R2 + r2];
             xa = make_double2(a0.x + a1.x, a0.y + a1.y);
             xb = make_double2(b0.x + b1.x, b0.y + b1.y);
         } else if (MODE == MODE_UPY) {    // w3, contiguous
-            xa = src[((size_t)node * n3 + c) * R2 + r2];
-            xb = src[((size_t)node * n3 + c + hc) * R2 + r2];
-        } else {                          // DOWN: u_ext gathered at the paired boundary rows
-            const int ca = sym_ext_a(c, acq);
-            xa = src[(size_t)a.xi0[(size_t)node * next + ca] * R2 + r2];
-            xb = src[(size_t)a.xi0[(size_t)node * next + ca + acq] * R2 + r2];
+            xa = src[((size_t)node * n3 + pa) * R2 + r2];
+            xb = src[((size_t)node * n3 + pb) * R2 + r2];
+        } else {                          // DOWN: u_ext gathered at the boundary positions
+            xa = src[(size_t)a.xi0[(size_t)node * next + pa] * R2 + r2];
+            xb = src[(size_t)a.xi0[(size_t)node * next + pb] * R2 + r2];
         }
-        xs[((nb * 2 + 0) * hc + c) * R2 + r2] = make_double2(xa.x + xb.x, xa.y + xb.y);
-        xs[((nb * 2 + 1) * hc + c) * R2 + r2] = make_double2(xa.x - xb.x, xa.y - xb.y);
+        const double s = sp.is[c];
+        xs[((nb * 2 + 0) * hc + c) * R2 + r2] = make_double2(xa.x + s * xb.x, xa.y + s * xb.y);
+        xs[((nb * 2 + 1) * hc + c) * R2 + r2] = make_double2(xa.x - s * xb.x, xa.y - s * xb.y);
     }
     __syncthreads();
     const int rl = threadIdx.x % a.RB;
@@ -552,28 +558,29 @@ __global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a) {
     }
     if (cs != 0 || row >= hr) return;
     double2* dst = a.ydst + (size_t)m * a.ydst_ps * R2;
+    const int ra = sp.oA[row], rbw = sp.oB[row];
+    const double so = 0.5 * sp.os[row];
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
         const int node = node0 + nb;
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
             const double2 yA = make_double2(0.5 * (ap[nb][r].x + am[nb][r].x), 0.5 * (ap[nb][r].y + am[nb][r].y));
-            const double2 yB = make_double2(0.5 * (ap[nb][r].x - am[nb][r].x), 0.5 * (ap[nb][r].y - am[nb][r].y));
+            const double2 yB = make_double2(so * (ap[nb][r].x - am[nb][r].x), so * (ap[nb][r].y - am[nb][r].y));
             if (MODE == MODE_UPX) {
-                dst[((size_t)node * n3 + row) * R2 + r] = yA;
-                dst[((size_t)node * n3 + row + hr) * R2 + r] = yB;
+                dst[((size_t)node * n3 + ra) * R2 + r] = yA;
+                dst[((size_t)node * n3 + rbw) * R2 + r] = yB;
             } else if (MODE == MODE_UPY) {
                 const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
-                const int ra = sym_ext_a(row, acq), rbw = ra + acq;
                 const double2* add = a.ysrc + (size_t)m * a.ysrc_ps * R2;
                 const double2 ea = add[(size_t)(base + a.yi[ra]) * R2 + r], eb = add[(size_t)(base + a.yi[rbw]) * R2 + r];
                 dst[((size_t)node * next + ra) * R2 + r] = make_double2(yA.x + ea.x, yA.y + ea.y);
                 dst[((size_t)node * next + rbw) * R2 + r] = make_double2(yB.x + eb.x, yB.y + eb.y);
             } else {
                 const double2* w3 = a.ysrc + (size_t)m * a.ysrc_ps * R2;
-                const double2 wa = w3[((size_t)node * n3 + row) * R2 + r], wb = w3[((size_t)node * n3 + row + hr) * R2 + r];
-                dst[(size_t)a.yo[(size_t)node * n3 + row] * R2 + r] = make_double2(yA.x + wa.x, yA.y + wa.y);
-                dst[(size_t)a.yo[(size_t)node * n3 + row + hr] * R2 + r] = make_double2(yB.x + wb.x, yB.y + wb.y);
+                const double2 wa = w3[((size_t)node * n3 + ra) * R2 + r], wb = w3[((size_t)node * n3 + rbw) * R2 + r];
+                dst[(size_t)a.yo[(size_t)node * n3 + ra] * R2 + r] = make_double2(yA.x + wa.x, yA.y + wa.y);
+                dst[(size_t)a.yo[(size_t)node * n3 + rbw] * R2 + r] = make_double2(yB.x + wb.x, yB.y + wb.y);
             }
         }
     }
@@ -1095,6 +1102,16 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         for (int i = 0; i < q; ++i)
             for (int j = 0; j < q; ++j) K[static_cast<size_t>(i) * q + j] = ch.D2[(i + 1) * p + (j + 1)];
         if ((rc = real_eig(q, K, lam, V, Vi))) return rc;
+        // parity of each eigenvector under i -> q-1-i (K commutes with the flip)
+        mode_parity.assign(q, 1.0);
+        for (int k = 0; k < q; ++k) {
+            double dp = 0.0, dm = 0.0;
+            for (int i = 0; i < q; ++i) {
+                dp += std::fabs(V[static_cast<size_t>(i) * q + k] - V[static_cast<size_t>(q - 1 - i) * q + k]);
+                dm += std::fabs(V[static_cast<size_t>(i) * q + k] + V[static_cast<size_t>(q - 1 - i) * q + k]);
+            }
+            mode_parity[k] = dp <= dm ? 1.0 : -1.0;
+        }
         std::vector<double> Vp(SP_T * SP_T, 0.0), Vip(SP_T * SP_T, 0.0);
         for (int i = 0; i < q; ++i)
             for (int j = 0; j < q; ++j) {
@@ -1174,10 +1191,11 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         D.nodes = L.nodes; D.n3 = L.n3; D.next = L.next; D.nchild = L.nchild; D.child_nodes = L.child_nodes;
         D.nbx = L.nbx; D.dir = L.dir;
         const size_t st = shared ? 1 : static_cast<size_t>(L.nodes);
-        // the cylinder level of the shared store keeps only the symmetric half pair
-        // [M+ | M-] of each operator (k_gemv_sym; GEMV-compatible R2 only)
-        D.sym = shared && (R2 == 2 || R2 == 4 || R2 == 8) && li + 1 == T.levels.size() && L.nodes == 2 &&
-                L.next == 2 * T.n * T.q && L.n3 % 2 == 0 && std::getenv("REXP_NO_SYM") == nullptr;
+        // top levels of the spectral shared store (few nodes: GEMV stages) keep only
+        // the symmetric half pair [M+ | M-] of each operator (k_gemv_sym)
+        D.sym = false;
+        if (fdm && (R2 == 2 || R2 == 4 || R2 == 8) && L.nodes * R2 <= 8 && li > 0 && std::getenv("REXP_NO_SYM") == nullptr)
+            if ((rc = sym_pairs(T, L, D))) return rc;   // sets D.sym when the pairing is a fixed-point-free involution
         D.ppX = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * (L.n3 / 2) : st * L.n3 * L.n3;
         D.ppY = D.sym ? 2 * static_cast<size_t>(L.next / 2) * (L.n3 / 2) : st * L.next * L.n3;
         D.ppS = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * (L.next / 2) : st * L.n3 * L.next;
@@ -1278,6 +1296,51 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     return tune_stages(false);
 }
 
+// Pairing of a level's interface and boundary positions (node 0) under the
+// reflection along its interface (x-merge: y -> b H - y, y-merge: x -> a H - x;
+// node 0's box has its origin at (0, 0)), in the spectral edge basis: slot k of
+// segment seg pairs with slot k of the mirror segment, sign = parity of mode k
+// if the reflection reverses the segment, else +1.  D.sym is set only if both
+// pairings are fixed-point-free involutions.
+int DeviceStore::sym_pairs(const Tree& T, const MergeLevel& L, Level& D) {
+    const double H = 1.0 / T.n;
+    auto wrapd = [](double v) { return std::fabs(v - std::floor(v + 0.5)); };
+    auto pairs = [&](const int32_t* gl, int cnt, std::vector<int>& A, std::vector<int>& B,
+                     std::vector<double>& S) -> bool {
+        std::vector<int> part(cnt, -1);
+        std::vector<double> sg(cnt, 1.0);
+        for (int r = 0; r < cnt; ++r) {
+            const double x = T.x[T.NI + gl[r]], y = T.y[T.NI + gl[r]];
+            const double mx = L.dir == 0 ? x : L.a * H - x, my = L.dir == 0 ? L.b * H - y : y;
+            int rm = -1;
+            for (int u = 0; u < cnt; ++u)
+                if (wrapd(T.x[T.NI + gl[u]] - mx) + wrapd(T.y[T.NI + gl[u]] - my) < 1e-9) { rm = u; break; }
+            if (rm < 0) return false;
+            const int k = r % q, km = rm % q;
+            if (km == k) sg[r] = 1.0;
+            else if (km == q - 1 - k) sg[r] = mode_parity[k];
+            else return false;
+            part[r] = (rm / q) * q + k;
+        }
+        for (int r = 0; r < cnt; ++r)
+            if (part[r] == r || part[part[r]] != r || sg[part[r]] != sg[r]) return false;
+        for (int r = 0; r < cnt; ++r)
+            if (r < part[r]) { A.push_back(r); B.push_back(part[r]); S.push_back(sg[r]); }
+        return static_cast<int>(A.size()) * 2 == cnt;
+    };
+    std::vector<int> iA, iB, eA, eB;
+    std::vector<double> is, es;
+    const bool ok = pairs(L.g3.data(), L.n3, iA, iB, is) && pairs(L.gext.data(), L.next, eA, eB, es);
+    if (!ok) return REXP_OK;
+    int rc;
+    if ((rc = put(&D.siA, iA)) || (rc = put(&D.siB, iB)) || (rc = put(&D.sis, is)) ||
+        (rc = put(&D.seA, eA)) || (rc = put(&D.seB, eB)) || (rc = put(&D.ses, es)))
+        return rc;
+    D.h_iA = iA; D.h_iB = iB; D.h_is = is; D.h_eA = eA; D.h_eB = eB; D.h_es = es;
+    D.sym = true;
+    return REXP_OK;
+}
+
 // copy the host factorization of local half poles [m0, m0 + count) into the store
 int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
     auto up = [&](const std::vector<cd>& v, double2* dst, size_t per_pole) -> int {
@@ -1299,39 +1362,29 @@ int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
     for (size_t li = 0; li < levels.size(); ++li) {
         Level& D = levels[li];
         if (D.sym) {
-            // [M+ | M-] per pole from the full (column-major) X, Y, S
-            const int n3 = D.n3, ne = D.next, h3 = n3 / 2, hx = ne / 2, acq = ne / 4;
-            auto ext_a = [acq](int c) { return c < acq ? c : acq + c; };
+            // [M+ | M-] per pole from the full (column-major) X, Y, S:
+            //   M+- (r, c) = A(A_r, A_c) +- s_c A(A_r, B_c)
+            const int n3 = D.n3, ne = D.next, h3 = n3 / 2, hx = ne / 2;
             const HostLevelOps& H = ops[li + 1];
             const size_t npole = H.m[0].size() / (static_cast<size_t>(n3) * n3);
             std::vector<cd> X2(npole * D.ppX), Y2(npole * D.ppY), S2(npole * D.ppS);
+            auto pair_op = [](const cd* M, int ld, int hrow, int hcol, const std::vector<int>& rA,
+                              const std::vector<int>& cA, const std::vector<int>& cB, const std::vector<double>& cs,
+                              cd* out) {
+                for (int c = 0; c < hcol; ++c)
+                    for (int r = 0; r < hrow; ++r) {
+                        const cd a11 = M[static_cast<size_t>(cA[c]) * ld + rA[r]];
+                        const cd a12 = cs[c] * M[static_cast<size_t>(cB[c]) * ld + rA[r]];
+                        out[static_cast<size_t>(c) * hrow + r] = a11 + a12;
+                        out[static_cast<size_t>(hrow) * hcol + static_cast<size_t>(c) * hrow + r] = a11 - a12;
+                    }
+            };
             for (size_t pl = 0; pl < npole; ++pl) {
-                const cd* X = H.m[0].data() + pl * n3 * n3;
-                const cd* Y = H.m[1].data() + pl * static_cast<size_t>(ne) * n3;
-                const cd* S = H.m[2].data() + pl * static_cast<size_t>(n3) * ne;
-                cd* xo = X2.data() + pl * D.ppX;
-                cd* yo = Y2.data() + pl * D.ppY;
-                cd* so = S2.data() + pl * D.ppS;
-                for (int c = 0; c < h3; ++c)        // X: rows mid, cols (mid, wrap)
-                    for (int r = 0; r < h3; ++r) {
-                        const cd a11 = X[static_cast<size_t>(c) * n3 + r], a12 = X[static_cast<size_t>(c + h3) * n3 + r];
-                        xo[static_cast<size_t>(c) * h3 + r] = a11 + a12;
-                        xo[static_cast<size_t>(h3) * h3 + static_cast<size_t>(c) * h3 + r] = a11 - a12;
-                    }
-                for (int c = 0; c < h3; ++c)        // Y: rows a-side ext, cols (mid, wrap)
-                    for (int r = 0; r < hx; ++r) {
-                        const int ra = ext_a(r);
-                        const cd a11 = Y[static_cast<size_t>(c) * ne + ra], a12 = Y[static_cast<size_t>(c + h3) * ne + ra];
-                        yo[static_cast<size_t>(c) * hx + r] = a11 + a12;
-                        yo[static_cast<size_t>(hx) * h3 + static_cast<size_t>(c) * hx + r] = a11 - a12;
-                    }
-                for (int c = 0; c < hx; ++c)        // S: rows mid, cols (a-side, b-side) ext
-                    for (int r = 0; r < h3; ++r) {
-                        const int ca = ext_a(c);
-                        const cd a11 = S[static_cast<size_t>(ca) * n3 + r], a12 = S[static_cast<size_t>(ca + acq) * n3 + r];
-                        so[static_cast<size_t>(c) * h3 + r] = a11 + a12;
-                        so[static_cast<size_t>(h3) * hx + static_cast<size_t>(c) * h3 + r] = a11 - a12;
-                    }
+                pair_op(H.m[0].data() + pl * n3 * n3, n3, h3, h3, D.h_iA, D.h_iA, D.h_iB, D.h_is, X2.data() + pl * D.ppX);
+                pair_op(H.m[1].data() + pl * static_cast<size_t>(ne) * n3, ne, hx, h3, D.h_eA, D.h_iA, D.h_iB, D.h_is,
+                        Y2.data() + pl * D.ppY);
+                pair_op(H.m[2].data() + pl * static_cast<size_t>(n3) * ne, n3, h3, hx, D.h_iA, D.h_eA, D.h_eB, D.h_es,
+                        S2.data() + pl * D.ppS);
             }
             if ((rc = up(X2, D.X, D.ppX))) return rc;
             if ((rc = up(Y2, D.Y, D.ppY))) return rc;
@@ -1402,24 +1455,24 @@ template <int R2>
 void allow_all() {
     allow_smem(k_gemv_sym<R2, 1, MODE_UPX>); allow_smem(k_gemv_sym<R2, 1, MODE_UPY>); allow_smem(k_gemv_sym<R2, 1, MODE_DOWN>);
     allow_smem(k_gemv_sym<R2, 2, MODE_UPX>); allow_smem(k_gemv_sym<R2, 2, MODE_UPY>); allow_smem(k_gemv_sym<R2, 2, MODE_DOWN>);
+    allow_smem(k_gemv_sym<R2, 4, MODE_UPX>); allow_smem(k_gemv_sym<R2, 4, MODE_UPY>); allow_smem(k_gemv_sym<R2, 4, MODE_DOWN>);
     allow_all_nb<R2, 1>();
     allow_all_nb<R2, 2>();
     allow_all_nb<R2, 4>();
     allow_all_nb<R2, 8>();
 }
 
+template <int R2, int MODE>
+void launch_gemv_sym_r(int NB, dim3 grid, size_t smem, cudaStream_t s, const GemvArgs& a, const SymPairs& p) {
+    if (NB >= 4) k_gemv_sym<R2, 4, MODE><<<grid, 256, smem, s>>>(a, p);
+    else if (NB == 2) k_gemv_sym<R2, 2, MODE><<<grid, 256, smem, s>>>(a, p);
+    else k_gemv_sym<R2, 1, MODE><<<grid, 256, smem, s>>>(a, p);
+}
 template <int MODE>
-void launch_gemv_sym(int R2, int NB, dim3 grid, size_t smem, cudaStream_t s, const GemvArgs& a) {
-    if (R2 == 2) {
-        if (NB == 2) k_gemv_sym<2, 2, MODE><<<grid, 256, smem, s>>>(a);
-        else k_gemv_sym<2, 1, MODE><<<grid, 256, smem, s>>>(a);
-    } else if (R2 == 4) {
-        if (NB == 2) k_gemv_sym<4, 2, MODE><<<grid, 256, smem, s>>>(a);
-        else k_gemv_sym<4, 1, MODE><<<grid, 256, smem, s>>>(a);
-    } else {
-        if (NB == 2) k_gemv_sym<8, 2, MODE><<<grid, 256, smem, s>>>(a);
-        else k_gemv_sym<8, 1, MODE><<<grid, 256, smem, s>>>(a);
-    }
+void launch_gemv_sym(int R2, int NB, dim3 grid, size_t smem, cudaStream_t s, const GemvArgs& a, const SymPairs& p) {
+    if (R2 == 2) launch_gemv_sym_r<2, MODE>(NB, grid, smem, s, a, p);
+    else if (R2 == 4) launch_gemv_sym_r<4, MODE>(NB, grid, smem, s, a, p);
+    else launch_gemv_sym_r<8, MODE>(NB, grid, smem, s, a, p);
 }
 
 GemvArgs gemv_shape(int rows, int cols, int nodes, bool shared, int rbmax = 64) {
@@ -1537,7 +1590,8 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     double2* hp = d_h[(li + 1) % 2];
     const int cls = kind == 2 ? T_MERGE_DOWN : T_MERGE_UP;
     if (L.sym) {
-        const int NB = pick_nb(L.nodes, R2, shared) >= 2 ? 2 : 1;
+        const int nbp = pick_nb(L.nodes, R2, shared);
+        const int NB = nbp >= 4 ? 4 : nbp >= 2 ? 2 : 1;
         const int h3 = L.n3 / 2, hx = L.next / 2;
         GemvArgs g;
         if (kind == 0) {
@@ -1556,13 +1610,18 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
             g.ydst = d_edge; g.ydst_ps = NE; g.yo = L.g3;
         }
         g.nbx = L.nbx; g.xdir = L.dir == 0 ? 1 : 0; g.nchild = L.nchild;
+        SymPairs sp{};
+        sp.n3 = L.n3; sp.next = L.next;
+        const bool in_int = kind != 2, out_int = kind != 1;
+        sp.iA = in_int ? L.siA : L.seA; sp.iB = in_int ? L.siB : L.seB; sp.is = in_int ? L.sis : L.ses;
+        sp.oA = out_int ? L.siA : L.seA; sp.oB = out_int ? L.siB : L.seB; sp.os = out_int ? L.sis : L.ses;
         const dim3 grid((L.nodes / NB) * g.nrowblk, pc);
         const size_t smem = (static_cast<size_t>(NB) * 2 * g.cols * R2 +
                              static_cast<size_t>(g.CS > 1 ? g.CS : 0) * g.RB * 2 * NB * R2) * sizeof(double2);
         tbeg(s);
-        if (kind == 0) launch_gemv_sym<MODE_UPX>(R2, NB, grid, smem, s, g);
-        else if (kind == 1) launch_gemv_sym<MODE_UPY>(R2, NB, grid, smem, s, g);
-        else launch_gemv_sym<MODE_DOWN>(R2, NB, grid, smem, s, g);
+        if (kind == 0) launch_gemv_sym<MODE_UPX>(R2, NB, grid, smem, s, g, sp);
+        else if (kind == 1) launch_gemv_sym<MODE_UPY>(R2, NB, grid, smem, s, g, sp);
+        else launch_gemv_sym<MODE_DOWN>(R2, NB, grid, smem, s, g, sp);
         tend(cls, s);
         return REXP_OK;
     }

@@ -20,7 +20,11 @@ struct StageCfg {
 
 struct Level {
     int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0, nbx = 1, dir = 0;
-    bool sym = false;   // cylinder level stored as the symmetric half pair [M+ | M-] (k_gemv_sym)
+    bool sym = false;   // stored as the symmetric half pair [M+ | M-] (k_gemv_sym, see sym_pairs)
+    int *siA = nullptr, *siB = nullptr, *seA = nullptr, *seB = nullptr;   // interface / boundary pairs
+    double *sis = nullptr, *ses = nullptr;                                 // their signs
+    std::vector<int> h_iA, h_iB, h_eA, h_eB;
+    std::vector<double> h_is, h_es;
     double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
     int *ia3 = nullptr, *ib3 = nullptr, *ext = nullptr, *gext = nullptr, *g3 = nullptr;
     double2* w3 = nullptr;                              // [chunk][nodes][n3][R2]
@@ -94,6 +98,8 @@ class DeviceStore {
     int nlanes = 1, cur_lane = 0;
     cudaEvent_t ev_fork = nullptr;
     void use_lane(int ln);
+    int sym_pairs(const Tree& T, const MergeLevel& L, Level& D);
+    std::vector<double> mode_parity;   // +-1: parity of eigenvector k of K under i -> q-1-i
     cudaGraphExec_t graph_exec = nullptr;
     const double* graph_state = nullptr;
     cudaStream_t cap_stream = nullptr;

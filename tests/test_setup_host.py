@@ -291,3 +291,50 @@ def test_cylinder_level_swap_symmetry(n):
         assert np.abs(Y[rA][:, h3:] - Y[rB][:, :h3]).max() <= tol * np.abs(Y).max()
         assert np.abs(S[:h3][:, rA] - S[h3:][:, rB]).max() <= tol * np.abs(S).max()
         assert np.abs(S[:h3][:, rB] - S[h3:][:, rA]).max() <= tol * np.abs(S).max()
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_merge_levels_reflection_symmetry(n):
+    """DESIGN.md §2 "symmetric pairs": with constant coefficients every merge
+    level is mapped onto itself by the reflection along its interface
+    (x-merge: y -> b H - y, y-merge: x -> a H - x about node 0's box), which
+    pairs the interface and boundary positions without fixed points; X, Y, S
+    commute with it.  Checked here in the nodal basis on the exported host
+    operators (the device applies the same pairing in the spectral edge basis,
+    where the reversal of a segment becomes the parity sign of each mode)."""
+    from paper_1402_5168_b200 import api
+    p = 6
+    h = api.setup("rsw", n=n, p=p, tau=0.2, delta=1e-10, Lambda=100.0, f=1.0, device=-1, store="shared")
+    x, y = h.node_coords()
+    NI = n * n * (p - 2) ** 2
+    H = 1.0 / n
+    nlev = api.export_num_levels(h)
+    ac = bc = 1
+    for lev in range(1, nlev - 1):
+        xmerge = (lev - 1) % 2 == 0
+        if xmerge:
+            ac *= 2
+        else:
+            bc *= 2
+        nodes, _, n3, ne, _ = api.export_level_info(h, lev)[:5]
+        g3 = api.export_index(h, lev, 4, nodes * n3)[:n3]
+        gext = api.export_index(h, lev, 3, nodes * ne)[:ne]
+
+        def mirror_pairs(gl):
+            X, Y = x[NI + gl], y[NI + gl]
+            MX, MY = (X, bc * H - Y) if xmerge else (ac * H - X, Y)
+            d = (np.abs((X[None, :] - MX[:, None] + 0.5) % 1.0 - 0.5) +
+                 np.abs((Y[None, :] - MY[:, None] + 0.5) % 1.0 - 0.5))
+            j = d.argmin(axis=1)
+            assert (d[np.arange(len(gl)), j] < 1e-9).all()
+            assert (j[j] == np.arange(len(gl))).all() and (j != np.arange(len(gl))).all()
+            return j
+
+        pi, pe = mirror_pairs(g3), mirror_pairs(gext)
+        for half in (0, h.num_half_poles - 1):
+            X = api.export_matrix(h, half, lev, 0, 0, n3, n3)
+            Y = api.export_matrix(h, half, lev, 0, 1, ne, n3)
+            S = api.export_matrix(h, half, lev, 0, 2, n3, ne)
+            assert np.abs(X[np.ix_(pi, pi)] - X).max() <= 1e-12 * np.abs(X).max()
+            assert np.abs(Y[np.ix_(pe, pi)] - Y).max() <= 1e-12 * np.abs(Y).max()
+            assert np.abs(S[np.ix_(pi, pe)] - S).max() <= 1e-12 * np.abs(S).max()
