@@ -1591,7 +1591,8 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     const int cls = kind == 2 ? T_MERGE_DOWN : T_MERGE_UP;
     if (L.sym) {
         const int nbp = pick_nb(L.nodes, R2, shared);
-        const int NB = nbp >= 4 ? 4 : nbp >= 2 ? 2 : 1;
+        int NB = nbp >= 4 ? 4 : nbp >= 2 ? 2 : 1;
+        if (cfg.nb > 0 && cfg.nb < NB) NB = cfg.nb;   // fewer nodes per CTA: more CTAs (operator reuse via L2)
         const int h3 = L.n3 / 2, hx = L.next / 2;
         GemvArgs g;
         if (kind == 0) {
@@ -1755,11 +1756,12 @@ int DeviceStore::tune_stages(bool measure) {
     auto tune = [&](int kind, size_t li, StageCfg& best) {
         std::vector<StageCfg> cands;
         if (kind != 3 && levels[li].sym) {
-            for (int rb : {32, 64, 128, 256}) {
-                StageCfg c;
-                c.kind = 2; c.rb = rb;
-                cands.push_back(c);
-            }
+            for (int nb : {0, 2, 1})
+                for (int rb : {32, 64, 128, 256}) {
+                    StageCfg c;
+                    c.kind = 2; c.rb = rb; c.nb = nb;
+                    cands.push_back(c);
+                }
             float bt = time_cfg(kind, li, best);
             for (const StageCfg& c : cands) {
                 const float t = time_cfg(kind, li, c);
@@ -1807,7 +1809,8 @@ int DeviceStore::tune_stages(bool measure) {
 
 std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
-        return c.kind == 2 ? "sym" + std::to_string(c.rb) : c.kind == 1 ? "gemv" + std::to_string(c.rb)
+        return c.kind == 2 ? "sym" + std::to_string(c.rb) + (c.nb ? "n" + std::to_string(c.nb) : "")
+                           : c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
                                  (c.minb == 4 ? "r" : c.minb == 3 ? "s3" : "");
     };

@@ -16,6 +16,7 @@ struct StageCfg {
     int MT = 4, WN = 8;
     int minb = 1;   // 4: register-capped variant (4 resident CTAs per SM)
     int rb = 64;    // GEMV row block (CS = 256 / rb column groups)
+    int nb = 0;     // symmetric-pair GEMV: nodes per CTA (0 = as many as fit)
 };
 
 struct Level {
