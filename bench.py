@@ -137,10 +137,12 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
     q2, e = q * q, n * n
     lv = tree_dims(n, q)
     per = lambda nodes: 1 if shared else nodes
-    # the top levels of the spectral shared store (nodes * R2 <= 8, not the first
-    # level) are applied in symmetric-pair form: half the operator bytes and flops
-    sym = shared and leaf == "spectral" and R2 in (2, 4, 8)
-    lv = [(nd, n3, nx, 0.5 if (sym and i > 0 and nd * R2 <= 8) else 1.0) for i, (nd, n3, nx) in enumerate(lv)]
+    # merge levels of the spectral shared store applied in symmetric-pair form
+    # (device.cu: nodes * R2 <= 8 or R2 >= 16, not the first level): half the
+    # operator bytes and flops
+    sym = shared and leaf == "spectral"
+    lv = [(nd, n3, nx, 0.5 if (sym and i > 0 and (nd * R2 <= 8 or R2 >= 16)) else 1.0)
+          for i, (nd, n3, nx) in enumerate(lv)]
     merge = {
         "merge_up": (sum(hf * nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx, hf in lv),
                      sum(hf * nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx, hf in lv)),

@@ -1,0 +1,214 @@
+// Symmetric-pair DMMA GEMM for the merge levels of the spectral shared store.
+//
+// A level whose reflection along the interface maps each child onto itself
+// acts on the edge data as a signed involution without fixed points (pairs
+// A <-> B with sign s, device.cu: DeviceStore::sym_pairs).  Every operator of
+// the level commutes with it, so the store keeps only the half pair
+// M+- = A_AA +- A_AB S ([M+ | M-], each hr x hk column-major) and the product
+// over all nodes' columns is two half-size GEMMs:
+//     B+- [k][col] = x_{A_k}(col) +- s_k x_{B_k}(col)
+//     P = M+ B+,  D = M- B-,   y_{A_r} = (P + D)/2,  y_{B_r} = s_r (P - D)/2.
+// Same tiling and DMMA scheme as k_cgemm (cgemm.cuh); A tiles of both halves by
+// cp.async, B formed from the mode's gathers through registers, double-buffered.
+#pragma once
+
+#include "cgemm.cuh"
+
+namespace rexp {
+namespace dev {
+
+struct CgemmSymArgs {
+    CgemmArgs g;              // A = [M+ | M-] per pole, rows = hr, K = hk, the mode's gathers
+    const int *iA, *iB;       // input pairs (k)
+    const double* is;
+    const int *oA, *oB;       // output pairs (rows)
+    const double* os;
+    int n3, next;             // full interface / boundary sizes of the level
+};
+
+struct BRawSym { double v[8]; };
+
+// x at full input position pos for column col: UPX s3 = h^a_3 + h^b_3 (two gathers),
+// UPY w3, DOWN u_ext
+template <int R2T, int MODE>
+__device__ __forceinline__ void cgs_fetch1(const CgemmSymArgs& s, int m, int pos, int node, int r2, double* out) {
+    const CgemmArgs& a = s.g;
+    const int R2 = R2T ? R2T : a.R2;
+    if (MODE == CG_UPX) {
+        const double2* src = a.src + (size_t)m * a.src_ps * R2;
+        const int base = cg_child_base(a, node);
+        const double2 v0 = src[(size_t)(base + a.bi0[pos]) * R2 + r2];
+        const double2 v1 = src[(size_t)(base + a.bi1[pos]) * R2 + r2];
+        out[0] = v0.x; out[1] = v0.y; out[2] = v1.x; out[3] = v1.y;
+    } else if (MODE == CG_UPY) {
+        const double2 v = a.src[(size_t)m * a.src_ps * R2 + ((size_t)node * s.n3 + pos) * R2 + r2];
+        out[0] = v.x; out[1] = v.y; out[2] = 0.0; out[3] = 0.0;
+    } else {   // DOWN
+        const double2 v = a.src[((size_t)m * a.src_ps + a.bi0[(size_t)node * s.next + pos]) * R2 + r2];
+        out[0] = v.x; out[1] = v.y; out[2] = 0.0; out[3] = 0.0;
+    }
+}
+
+template <int MT, int WN, int BK, int WM = 1>
+constexpr size_t cgemm_sym_smem_bytes() {
+    return 4 * (size_t)BK * ((8 * MT * WM + 2) + (8 * WN + 2)) * sizeof(double2);
+}
+
+template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1>
+__global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
+    const CgemmArgs& a = s.g;
+    constexpr int BM = 8 * MT * WM, BN = 8 * WN, NT = 32 * WN * WM;
+    const int R2 = R2T ? R2T : a.R2;
+    constexpr int LDA = BM + 2, LDB = BN + 2;
+    constexpr int BPT = (BK * BN + NT - 1) / NT;
+    extern __shared__ double2 sm[];
+
+    const int m = blockIdx.y;
+    const int rb = blockIdx.x % a.nrowblk;
+    const int cb = blockIdx.x / a.nrowblk;
+    const int row0 = rb * BM, col0 = cb * BN;
+    const int ncols = a.nodes * R2;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int warp = wid % WN, wm = wid / WN;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int mrow0 = wm * MT * 8;
+    const int hr = a.rows, hk = a.K;
+    const double2* Ap = a.A + (size_t)m * 2 * hr * hk;   // M+
+    const double2* Am = Ap + (size_t)hr * hk;            // M-
+
+    // buffers: [buf][half] A tiles, then [buf][half] B tiles
+    auto As = [&](int buf, int hf) { return sm + (buf * 2 + hf) * BK * LDA; };
+    auto Bs = [&](int buf, int hf) { return sm + 4 * BK * LDA + (buf * 2 + hf) * BK * LDB; };
+
+    auto issue_A = [&](int buf, int k0) {
+        for (int e = tid; e < 2 * BK * BM; e += NT) {
+            const int hf = e / (BK * BM), ee = e % (BK * BM);
+            const int kk = ee / BM, r = ee % BM;
+            const int row = row0 + r, k = k0 + kk;
+            double2* base = As(buf, hf);
+            const double2* M = hf ? Am : Ap;
+            if (row < hr && k < hk) cp_async16(base + kk * LDA + r, M + (size_t)k * hr + row);
+            else base[kk * LDA + r] = make_double2(0.0, 0.0);
+        }
+        cp_async_commit();
+    };
+    BRawSym braw[BPT];
+    auto fetch_B = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < BPT; ++u) {
+            const int e = tid + u * NT;
+            const int kk = e / BN, c = e % BN;
+            const int k = k0 + kk, col = col0 + c;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) braw[u].v[j] = 0.0;
+            if (e < BK * BN && k < hk && col < ncols) {
+                const int node = col / R2, r2 = col % R2;
+                cgs_fetch1<R2T, MODE>(s, m, s.iA[k], node, r2, braw[u].v);
+                cgs_fetch1<R2T, MODE>(s, m, s.iB[k], node, r2, braw[u].v + 4);
+            }
+        }
+    };
+    auto store_B = [&](int buf, int k0) {
+#pragma unroll
+        for (int u = 0; u < BPT; ++u) {
+            const int e = tid + u * NT;
+            if (e < BK * BN) {
+                const int kk = e / BN, c = e % BN;
+                const int k = k0 + kk;
+                const double sg = k < hk ? s.is[k] : 0.0;
+                const double* v = braw[u].v;
+                const double xar = v[0] + v[2], xai = v[1] + v[3];   // UPX: two-child sum (others: v[2], v[3] = 0)
+                const double xbr = v[4] + v[6], xbi = v[5] + v[7];
+                Bs(buf, 0)[kk * LDB + c] = make_double2(xar + sg * xbr, xai + sg * xbi);
+                Bs(buf, 1)[kk * LDB + c] = make_double2(xar - sg * xbr, xai - sg * xbi);
+            }
+        }
+    };
+
+    double acc[2][MT][4];
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+        for (int i = 0; i < MT; ++i) acc[hf][i][0] = acc[hf][i][1] = acc[hf][i][2] = acc[hf][i][3] = 0.0;
+
+    const int nchunks = (hk + BK - 1) / BK;
+    issue_A(0, 0);
+    fetch_B(0);
+    store_B(0, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int buf = ch & 1;
+        const bool more = ch + 1 < nchunks;
+        if (more) {
+            issue_A(buf ^ 1, (ch + 1) * BK);
+            fetch_B((ch + 1) * BK);
+        }
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            const double2* Ab = As(buf, hf);
+            const double2* Bb = Bs(buf, hf);
+#pragma unroll
+            for (int ks = 0; ks < BK / 4; ++ks) {
+                const int kk = ks * 4 + t4;
+                const double2 b = Bb[kk * LDB + warp * 8 + g];
+                double2 av[MT];
+#pragma unroll
+                for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + mrow0 + i * 8 + g];
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][0], acc[hf][i][1], av[i].x, b.x);
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][2], acc[hf][i][3], av[i].x, b.y);
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][0], acc[hf][i][1], av[i].y, -b.y);
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][2], acc[hf][i][3], av[i].y, b.x);
+            }
+        }
+        if (more) {
+            store_B(buf ^ 1, (ch + 1) * BK);
+            cp_async_wait_all();
+        }
+        __syncthreads();
+    }
+    // epilogue: half row rr -> rows oA[rr] (y_A) and oB[rr] (y_B)
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const int rr = row0 + mrow0 + i * 8 + g;
+        if (rr >= hr) continue;
+        const int ra = s.oA[rr], rbw = s.oB[rr];
+        const double so = 0.5 * s.os[rr];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int col = col0 + warp * 8 + 2 * t4 + j;
+            if (col >= ncols) continue;
+            const int node = col / R2, r2 = col % R2;
+            const double pr = acc[0][i][j], pi = acc[0][i][2 + j], dr = acc[1][i][j], di = acc[1][i][2 + j];
+            double2 yA = make_double2(0.5 * (pr + dr), 0.5 * (pi + di));
+            double2 yB = make_double2(so * (pr - dr), so * (pi - di));
+            if (MODE == CG_UPX) {
+                double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
+                dst[((size_t)node * s.n3 + ra) * R2 + r2] = yA;
+                dst[((size_t)node * s.n3 + rbw) * R2 + r2] = yB;
+            } else if (MODE == CG_UPY) {
+                const int base = cg_child_base(a, node);
+                const double2 ea = a.add[((size_t)m * a.add_ps + base + a.ai0[ra]) * R2 + r2];
+                const double2 eb = a.add[((size_t)m * a.add_ps + base + a.ai0[rbw]) * R2 + r2];
+                double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
+                dst[((size_t)node * s.next + ra) * R2 + r2] = make_double2(yA.x + ea.x, yA.y + ea.y);
+                dst[((size_t)node * s.next + rbw) * R2 + r2] = make_double2(yB.x + eb.x, yB.y + eb.y);
+            } else {   // DOWN: u3 = y + w3, scattered to the edge array
+                const double2* w3 = a.add + (size_t)m * a.add_ps * R2;
+                const double2 wa = w3[((size_t)node * s.n3 + ra) * R2 + r2];
+                const double2 wb = w3[((size_t)node * s.n3 + rbw) * R2 + r2];
+                a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + ra]) * R2 + r2] =
+                    make_double2(yA.x + wa.x, yA.y + wa.y);
+                a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + rbw]) * R2 + r2] =
+                    make_double2(yB.x + wb.x, yB.y + wb.y);
+            }
+        }
+    }
+}
+
+}  // namespace dev
+}  // namespace rexp

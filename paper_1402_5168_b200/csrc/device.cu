@@ -27,10 +27,14 @@
 #include "rexp_device.hpp"
 #include "cgemm.cuh"
 #include "cgemm_launch.hpp"
+#include "cgemm_sym.cuh"
 #include "leaf_spec.cuh"
 
 namespace rexp {
 namespace dev {
+
+void cgs_run(int mode, int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a);
+void cgs_allow();
 
 __device__ __forceinline__ void cfma(double2& acc, const double2 a, const double2 b) {
     acc.x = fma(a.x, b.x, acc.x);
@@ -1194,7 +1198,10 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         // top levels of the spectral shared store (few nodes: GEMV stages) keep only
         // the symmetric half pair [M+ | M-] of each operator (k_gemv_sym)
         D.sym = false;
-        if (fdm && (R2 == 2 || R2 == 4 || R2 == 8) && L.nodes * R2 <= 8 && li > 0 && std::getenv("REXP_NO_SYM") == nullptr)
+        // pair form where it pays: GEMV levels (few nodes) and, with many right-hand
+        // sides, every GEMM level (compute-bound: half the FP64 work); the
+        // latency-bound low levels of few-RHS runs keep the full GEMM
+        if (fdm && li > 0 && (L.nodes * R2 <= 8 || R2 >= 16) && std::getenv("REXP_NO_SYM") == nullptr)
             if ((rc = sym_pairs(T, L, D))) return rc;   // sets D.sym when the pairing is a fixed-point-free involution
         D.ppX = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * (L.n3 / 2) : st * L.n3 * L.n3;
         D.ppY = D.sym ? 2 * static_cast<size_t>(L.next / 2) * (L.n3 / 2) : st * L.next * L.n3;
@@ -1521,6 +1528,7 @@ void DeviceStore::configure_kernels() {
     cg_allow_all();
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cgs_allow();
     cudaFuncSetAttribute(k_leaf_spec_down, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_leaf_spec_up, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
@@ -1589,6 +1597,42 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     const double2* hc = d_h[li % 2];
     double2* hp = d_h[(li + 1) % 2];
     const int cls = kind == 2 ? T_MERGE_DOWN : T_MERGE_UP;
+    if (L.sym && cfg.kind == 3) {
+        CgemmSymArgs sa{};
+        CgemmArgs& a = sa.g;
+        a.nodes = L.nodes; a.R2 = R2;
+        a.nbx = L.nbx; a.xdir = L.dir == 0 ? 1 : 0; a.nchild = L.nchild;
+        const int h3 = L.n3 / 2, hx = L.next / 2;
+        int mode;
+        if (kind == 0) {
+            mode = CG_UPX;
+            a.A = L.X + static_cast<size_t>(m0) * L.ppX; a.rows = h3; a.K = h3;
+            a.src = hc; a.src_ps = hstride; a.bi0 = L.ia3; a.bi1 = L.ib3;
+            a.dst = L.w3; a.dst_ps = static_cast<long long>(L.nodes) * L.n3;
+        } else if (kind == 1) {
+            mode = CG_UPY;
+            a.A = L.Y + static_cast<size_t>(m0) * L.ppY; a.rows = hx; a.K = h3;
+            a.src = L.w3; a.src_ps = static_cast<long long>(L.nodes) * L.n3;
+            a.dst = hp; a.dst_ps = hstride; a.add = hc; a.add_ps = hstride; a.ai0 = L.ext;
+        } else {
+            mode = CG_DOWN;
+            a.A = L.S + static_cast<size_t>(m0) * L.ppS; a.rows = h3; a.K = hx;
+            a.src = d_edge; a.src_ps = NE; a.bi0 = L.gext;
+            a.add = L.w3; a.add_ps = static_cast<long long>(L.nodes) * L.n3;
+            a.dst = d_edge; a.dst_ps = NE; a.so0 = L.g3;
+        }
+        const bool in_int = kind != 2, out_int = kind != 1;
+        sa.iA = in_int ? L.siA : L.seA; sa.iB = in_int ? L.siB : L.seB; sa.is = in_int ? L.sis : L.ses;
+        sa.oA = out_int ? L.siA : L.seA; sa.oB = out_int ? L.siB : L.seB; sa.os = out_int ? L.sis : L.ses;
+        sa.n3 = L.n3; sa.next = L.next;
+        const int bm = 8 * cfg.MT * cg_wm(cfg.WN);
+        a.nrowblk = (a.rows + bm - 1) / bm;
+        const int ncb = (L.nodes * R2 + 8 * cfg.WN - 1) / (8 * cfg.WN);
+        tbeg(s);
+        cgs_run(mode, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, sa);
+        tend(cls, s);
+        return REXP_OK;
+    }
     if (L.sym) {
         const int nbp = pick_nb(L.nodes, R2, shared);
         int NB = nbp >= 4 ? 4 : nbp >= 2 ? 2 : 1;
@@ -1697,7 +1741,7 @@ int DeviceStore::tune_stages(bool measure) {
         const Level& L = levels[li];
         const bool use_gemm = shared && (L.nodes * R2 >= 4 || !gemv_ok);
         StageCfg c;
-        c.kind = L.sym ? 2 : use_gemm ? 0 : 1;
+        c.kind = L.sym ? (gemv_ok && L.nodes * R2 <= 8 ? 2 : 3) : use_gemm ? 0 : 1;
         cg_tile(L.n3, L.nodes * R2, c.MT, c.WN);
         t_upx[li] = c;
         t_down[li] = c;
@@ -1756,10 +1800,17 @@ int DeviceStore::tune_stages(bool measure) {
     auto tune = [&](int kind, size_t li, StageCfg& best) {
         std::vector<StageCfg> cands;
         if (kind != 3 && levels[li].sym) {
-            for (int nb : {0, 2, 1})
-                for (int rb : {32, 64, 128, 256}) {
+            if (gemv_ok)
+                for (int nb : {0, 2, 1})
+                    for (int rb : {32, 64, 128, 256}) {
+                        StageCfg c;
+                        c.kind = 2; c.rb = rb; c.nb = nb;
+                        cands.push_back(c);
+                    }
+            for (int mt : {2, 4})
+                for (int wn : {2, 4, 8}) {
                     StageCfg c;
-                    c.kind = 2; c.rb = rb; c.nb = nb;
+                    c.kind = 3; c.MT = mt; c.WN = wn;
                     cands.push_back(c);
                 }
             float bt = time_cfg(kind, li, best);
@@ -1809,6 +1860,7 @@ int DeviceStore::tune_stages(bool measure) {
 
 std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
+        if (c.kind == 3) return "symgemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN);
         return c.kind == 2 ? "sym" + std::to_string(c.rb) + (c.nb ? "n" + std::to_string(c.nb) : "")
                            : c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
