@@ -1529,8 +1529,10 @@ void DeviceStore::configure_kernels() {
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cgs_allow();
-    cudaFuncSetAttribute(k_leaf_spec_down, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_spec_up, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_spec_down<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_spec_up<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_spec_down<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_spec_up<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
@@ -1883,7 +1885,8 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     const dim3 sp_grid(static_cast<unsigned>(nelem * nrhs), static_cast<unsigned>(sp.ngroups));
     if (fdm) {
         tbeg(s);
-        k_leaf_spec_up<<<sp_grid, SP_THREADS, sp_up_smem(), s>>>(sp);
+        if (q == 14) k_leaf_spec_up<14><<<sp_grid, SP_THREADS, sp_up_smem(), s>>>(sp);
+        else k_leaf_spec_up<0><<<sp_grid, SP_THREADS, sp_up_smem(), s>>>(sp);
         tend(T_LEAF_UP, s);
     } else if (shared) {
         CgemmArgs a{};
@@ -1936,7 +1939,8 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     // ---- leaves down ----
     if (fdm) {
         tbeg(s);
-        k_leaf_spec_down<<<sp_grid, SP_THREADS, sp_down_smem(), s>>>(sp);
+        if (q == 14) k_leaf_spec_down<14><<<sp_grid, SP_THREADS, sp_down_smem(), s>>>(sp);
+        else k_leaf_spec_down<0><<<sp_grid, SP_THREADS, sp_down_smem(), s>>>(sp);
         tend(T_LEAF_DOWN, s);
     } else if (shared) {
         CgemmArgs a{};

@@ -124,13 +124,16 @@ constexpr size_t sp_up_smem() {
            2 * SP_T * sizeof(double);
 }
 
+// QT: compile-time q (0 = runtime a.q); q = 14 (p = 16) is instantiated so the
+// per-pole loops have constant trip counts
+template <int QT>
 __global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
     extern __shared__ double2 usm[];
     double2* Ds = usm;                                   // [2][SP_PB][256] Dinv rows (cp.async, one batch ahead)
     double2* Ws = Ds + 2 * SP_PB * SP_T * SP_T;          // [SP_PB][2][SP_T * SP_LW] W[i'][j'] at j'*SP_LW + i'
     double2* cfs = Ws + SP_PB * 2 * SP_T * SP_LW;        // [2][SP_PB][4] c_mf
     double* es = reinterpret_cast<double*>(cfs + 2 * SP_PB * 4);
-    const int q = a.q, nbnd = 4 * q, t = threadIdx.x;
+    const int q = QT ? QT : a.q, nbnd = 4 * q, t = threadIdx.x;
     const int nrhs = a.R2 / 2;
     const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
     int m0, m1;
@@ -252,13 +255,14 @@ constexpr size_t sp_down_smem() {
            2 * SP_T * sizeof(double);
 }
 
+template <int QT>
 __global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
     extern __shared__ double2 dsm[];
     double2* UBs = dsm;                                  // [2][SP_PB][2][SP_NB] edge-basis boundary values
     double2* Ds = UBs + 2 * SP_UBN;                      // [2][SP_PB][256] Dinv rows
     double2* dEs = Ds + 2 * SP_PB * SP_T * SP_T;         // [2][SP_PB][4]   d_mk
     double* as = reinterpret_cast<double*>(dEs + 2 * SP_PB * 4);
-    const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
+    const int q = QT ? QT : a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
     const int nrhs = a.R2 / 2;
     const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
     const int grp = blockIdx.y;
