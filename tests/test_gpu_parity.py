@@ -87,7 +87,7 @@ def test_config0_nrhs2_and_host_path(c0):
     h.close()
 
 
-@pytest.mark.parametrize("nrhs,chunk", [(8, "37"), (3, "1000")])
+@pytest.mark.parametrize("nrhs,chunk", [(8, "37"), (3, "1000"), (4, "1000")])
 def test_config0_many_rhs_and_pole_chunks(c0, nrhs, chunk, monkeypatch):
     """Multi-RHS path (config 3's shape at config 0 size): nrhs independent states,
     runtime-R2 DMMA GEMMs at every level incl. the periodic closure, and the pole
