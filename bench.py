@@ -131,7 +131,7 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
             owned edge segments' pole sums                    2q * 4 nE
     (the RHS-field part of the pole sum is pole-independent, sum_m Re(d_mk c_mf
     Dinv_m) =: Pi_kf, applied once per step in k_spec_back).  The once-per-step
-    transforms (k_spec_pre, k_spec_back) are O(q^3) per leaf, not per pole.
+    transforms (k_spec_pre_fused, k_spec_back) are O(q^3) per leaf, not per pole.
     """
     n, q = cfg["n"], cfg["p"] - 2
     q2, e = q * q, n * n

@@ -1542,7 +1542,7 @@ int DeviceStore::launches_per_step() const {
     int nchunks = 0;
     for (const auto& B : lane_bufs) nchunks += (B.m1 - B.m0 + chunk - 1) / chunk;
     const int per_chunk = (shared && !fdm ? 5 : 4) + 3 * static_cast<int>(levels.size());
-    return fdm ? 4 + nchunks * (3 + 3 * static_cast<int>(levels.size())) : 2 + nchunks * per_chunk;
+    return fdm ? 3 + nchunks * (3 + 3 * static_cast<int>(levels.size())) : 2 + nchunks * per_chunk;
 }
 
 int DeviceStore::check(const char* what) {
@@ -2004,19 +2004,20 @@ int DeviceStore::pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out
 }
 
 int DeviceStore::solve_sum(const double* d_state, double* d_E_out, cudaStream_t s) {
-    {
+    if (fdm) {
+        // spectral path (RSW): RHS fields and their spectral coefficients in one kernel
+        SpecArgs sp = spec_args(0, chunk);
+        sp.u = d_state; sp.elem_g = d_elem_g; sp.Dm = d_D;
+        tbeg(s);
+        k_spec_pre_fused<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
+        tend(T_PRE, s);
+    } else {
         PreArgs a{};
         a.u = d_state; a.F = d_F; a.elem_g = d_elem_g; a.D = d_D; a.kappa = d_kappa;
         a.model = model; a.n = n; a.p = p; a.q = q; a.R2 = R2; a.nF = nF; a.N = N; a.NI = NI; a.c1 = c1;
         const long long tot = NI * R2;
         tbeg(s);
         k_pre<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
-        tend(T_PRE, s);
-    }
-    if (fdm) {
-        SpecArgs sp = spec_args(0, chunk);
-        tbeg(s);
-        k_spec_pre<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
         tend(T_PRE, s);
     }
     int rc;

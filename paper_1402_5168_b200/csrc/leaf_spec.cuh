@@ -7,7 +7,7 @@
 //     A_II^{-1} T = V W V^T,   W = (V^-1 T V^-T) ./ (c2 (l_i + l_j) - sigma_m).
 // Everything pole-dependent is elementwise in the spectral basis, so the
 // O(q^3) transforms are hoisted out of the pole loop:
-//   * RHS fields:   G_f = V^-1 F_f V^-T once per step (k_spec_pre), and
+//   * RHS fields:   G_f = V^-1 F_f V^-T once per step (k_spec_pre_fused), and
 //                   V^-1 (sum_f c_mf F_f) V^-T = sum_f c_mf G_f;
 //   * boundary:     A_IB u_B is a sum of four outer products a (x) u_side, so
 //                   V^-1 (A_IB u_B) V^-T = c2 (a0^ ul^T + a1^ ur^T + ub^ a0^T + ut^ a1^T)
@@ -60,6 +60,10 @@ struct SpecArgs {
     // BACK
     double* E;              // [nE][R2][N]
     long long N;
+    // fused RHS fields (k_spec_pre_fused)
+    const double* u;        // state [nrhs][3][N] complex interleaved
+    const int* elem_g;      // [nelem][p*p] (-1 at corners)
+    const double* Dm;       // p x p differentiation matrix
 };
 
 __device__ __forceinline__ void sp_group_range(const SpecArgs& a, int grp, int& m0, int& m1) {
@@ -69,34 +73,55 @@ __device__ __forceinline__ void sp_group_range(const SpecArgs& a, int grp, int& 
 }
 
 // --------------------------------------------------------------------------
-// k_spec_pre: G_f = V^-1 F_f V^-T   (grid: nelem * R2 CTAs)
+// k_spec_pre_fused: RSW RHS fields at the leaf's interior nodes (§2.1,
+// eta0, div v0, curl v0 from the element's nodal values, R8) straight into
+// their spectral coefficients G_f = V^-1 F_f V^-T (grid: nelem * R2 CTAs)
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(SP_THREADS) k_spec_pre(SpecArgs a) {
+__global__ void __launch_bounds__(SP_THREADS) k_spec_pre_fused(SpecArgs a) {
+    constexpr int PM = SP_T + 2;                       // p <= 18
+    __shared__ double us[3][PM * PM];                  // v1, v2, eta at the element's p x p nodes
+    __shared__ double ds[PM * PM];
     __shared__ double fs[3][SP_T * SP_T];
     __shared__ double ts[3][SP_T * SP_T];
     __shared__ double vis[SP_T * (SP_T + 1)];
-    const int q = a.q, q2 = q * q, t = threadIdx.x;
+    const int q = a.q, p = a.p, q2 = q * q, t = threadIdx.x;
     const int leaf = blockIdx.x / a.R2, r2 = blockIdx.x % a.R2;
+    const int k = r2 >> 1, part = r2 & 1;
     for (int e = t; e < SP_T * SP_T; e += blockDim.x) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
-    for (int e = t; e < a.nF * q2; e += blockDim.x) {
-        const int f = e / q2, node = e % q2;   // node = j*q + i
-        fs[f][node] = a.F[((size_t)r2 * a.nF + f) * ((size_t)a.nelem * q2) + (size_t)leaf * q2 + node];
+    for (int e = t; e < p * p; e += blockDim.x) ds[e] = a.Dm[e];
+    for (int e = t; e < 3 * p * p; e += blockDim.x) {
+        const int fld = e / (p * p), node = e % (p * p);
+        const int g = a.elem_g[(size_t)leaf * p * p + node];
+        us[fld][node] = g >= 0 ? a.u[(((size_t)k * 3 + fld) * a.N + g) * 2 + part] : 0.0;
     }
     __syncthreads();
-    // T1[f][(j, i')] = sum_i Vinv[i'][i] F_f[i][j]
-    for (int e = t; e < a.nF * q2; e += blockDim.x) {
+    for (int e = t; e < q2; e += blockDim.x) {
+        const int i = e % q + 1, j = e / q + 1;        // interior node (i, j), node index j*p + i
+        double dx0 = 0.0, dx1 = 0.0, dy0 = 0.0, dy1 = 0.0;
+        for (int kk = 0; kk < p; ++kk) {
+            const double dxw = ds[i * p + kk], dyw = ds[j * p + kk];
+            dx0 = fma(dxw, us[0][j * p + kk], dx0);
+            dx1 = fma(dxw, us[1][j * p + kk], dx1);
+            dy0 = fma(dyw, us[0][kk * p + i], dy0);
+            dy1 = fma(dyw, us[1][kk * p + i], dy1);
+        }
+        fs[0][e] = us[2][j * p + i];
+        fs[1][e] = a.c1 * (dx0 + dy1);
+        fs[2][e] = a.c1 * (dx1 - dy0);
+    }
+    __syncthreads();
+    for (int e = t; e < 3 * q2; e += blockDim.x) {
         const int f = e / q2, node = e % q2, ip = node % q, j = node / q;
-        double s = 0.0;
-        for (int i = 0; i < q; ++i) s = fma(vis[ip * (SP_T + 1) + i], fs[f][j * q + i], s);
-        ts[f][j * q + ip] = s;
+        double sum = 0.0;
+        for (int i = 0; i < q; ++i) sum = fma(vis[ip * (SP_T + 1) + i], fs[f][j * q + i], sum);
+        ts[f][j * q + ip] = sum;
     }
     __syncthreads();
-    // G_f[(j', i')] = sum_j T1[f][(j, i')] Vinv[j'][j]
-    for (int e = t; e < a.nF * q2; e += blockDim.x) {
+    for (int e = t; e < 3 * q2; e += blockDim.x) {
         const int f = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
-        double s = 0.0;
-        for (int j = 0; j < q; ++j) s = fma(ts[f][j * q + ip], vis[jp * (SP_T + 1) + j], s);
-        a.G[(((size_t)leaf * a.R2 + r2) * a.nF + f) * q2 + mode] = s;
+        double sum = 0.0;
+        for (int j = 0; j < q; ++j) sum = fma(ts[f][j * q + ip], vis[jp * (SP_T + 1) + j], sum);
+        a.G[(((size_t)leaf * a.R2 + r2) * a.nF + f) * q2 + mode] = sum;
     }
 }
 
