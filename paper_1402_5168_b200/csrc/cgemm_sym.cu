@@ -6,61 +6,74 @@ namespace rexp {
 namespace dev {
 namespace {
 
-template <int MT, int WN, int BK, int R2T, int MODE>
+template <int MT, int WN, int BK, int R2T, int MODE, int NST>
 void cgs_launch(dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
     constexpr int WM = WN == 2 ? 4 : WN == 4 ? 2 : 1;
-    k_cgemm_sym<MT, WN, BK, R2T, MODE, WM><<<grid, 32 * WN * WM, cgemm_sym_smem_bytes<MT, WN, BK, WM>(), s>>>(a);
+    k_cgemm_sym<MT, WN, BK, R2T, MODE, WM, NST>
+        <<<grid, 32 * WN * WM, cgemm_sym_smem_bytes<MT, WN, BK, WM, NST>(), s>>>(a);
 }
-template <int MT, int WN, int BK, int R2T, int MODE>
+template <int MT, int WN, int BK, int R2T, int MODE, int NST>
 void cgs_allow1() {
     constexpr int WM = WN == 2 ? 4 : WN == 4 ? 2 : 1;
-    cudaFuncSetAttribute(k_cgemm_sym<MT, WN, BK, R2T, MODE, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_cgemm_sym<MT, WN, BK, R2T, MODE, WM, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
 }
-template <int BK, int R2T, int MODE>
-void cgs_tiles(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
+template <int BK, int R2T, int MODE, int NST>
+void cgs_tiles_n(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
     if (MT == 2) {
-        if (WN == 2) cgs_launch<2, 2, BK, R2T, MODE>(grid, s, a);
-        else if (WN == 4) cgs_launch<2, 4, BK, R2T, MODE>(grid, s, a);
-        else cgs_launch<2, 8, BK, R2T, MODE>(grid, s, a);
+        if (WN == 2) cgs_launch<2, 2, BK, R2T, MODE, NST>(grid, s, a);
+        else if (WN == 4) cgs_launch<2, 4, BK, R2T, MODE, NST>(grid, s, a);
+        else cgs_launch<2, 8, BK, R2T, MODE, NST>(grid, s, a);
     } else {
-        if (WN == 2) cgs_launch<4, 2, BK, R2T, MODE>(grid, s, a);
-        else if (WN == 4) cgs_launch<4, 4, BK, R2T, MODE>(grid, s, a);
-        else cgs_launch<4, 8, BK, R2T, MODE>(grid, s, a);
+        if (WN == 2) cgs_launch<4, 2, BK, R2T, MODE, NST>(grid, s, a);
+        else if (WN == 4) cgs_launch<4, 4, BK, R2T, MODE, NST>(grid, s, a);
+        else cgs_launch<4, 8, BK, R2T, MODE, NST>(grid, s, a);
     }
+}
+// nst = 3: 3-stage cp.async ring (UP-Y / DOWN only)
+template <int BK, int R2T, int MODE>
+void cgs_tiles(int MT, int WN, int nst, dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
+    if constexpr (MODE == CG_UPY || MODE == CG_DOWN) {
+        if (nst >= 3) {
+            cgs_tiles_n<BK, R2T, MODE, 3>(MT, WN, grid, s, a);
+            return;
+        }
+    }
+    cgs_tiles_n<BK, R2T, MODE, 2>(MT, WN, grid, s, a);
+}
+template <int BK, int R2T, int MODE, int NST>
+void cgs_allow_n() {
+    cgs_allow1<2, 2, BK, R2T, MODE, NST>(); cgs_allow1<2, 4, BK, R2T, MODE, NST>(); cgs_allow1<2, 8, BK, R2T, MODE, NST>();
+    cgs_allow1<4, 2, BK, R2T, MODE, NST>(); cgs_allow1<4, 4, BK, R2T, MODE, NST>(); cgs_allow1<4, 8, BK, R2T, MODE, NST>();
 }
 template <int BK, int R2T, int MODE>
 void cgs_allow_tiles() {
-    cgs_allow1<2, 2, BK, R2T, MODE>(); cgs_allow1<2, 4, BK, R2T, MODE>(); cgs_allow1<2, 8, BK, R2T, MODE>();
-    cgs_allow1<4, 2, BK, R2T, MODE>(); cgs_allow1<4, 4, BK, R2T, MODE>(); cgs_allow1<4, 8, BK, R2T, MODE>();
+    cgs_allow_n<BK, R2T, MODE, 2>();
+    if constexpr (MODE == CG_UPY || MODE == CG_DOWN) cgs_allow_n<BK, R2T, MODE, 3>();
 }
+// BK = 16 always: the pair kernel stages A and B for both halves, so the
+// smaller chunk keeps two or more CTAs per SM (BK = 28 with 64-row tiles needs
+// ~180 KB of shared memory)
 template <int MODE>
-void cgs_run_mode(int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
-    const bool b28 = (K % 28) == 0;
-    if (R2 == 2) {
-        if (b28) cgs_tiles<28, 2, MODE>(MT, WN, grid, s, a);
-        else cgs_tiles<16, 2, MODE>(MT, WN, grid, s, a);
-    } else if (R2 == 4) {
-        if (b28) cgs_tiles<28, 4, MODE>(MT, WN, grid, s, a);
-        else cgs_tiles<16, 4, MODE>(MT, WN, grid, s, a);
-    } else {
-        if (b28) cgs_tiles<28, 0, MODE>(MT, WN, grid, s, a);
-        else cgs_tiles<16, 0, MODE>(MT, WN, grid, s, a);
-    }
+void cgs_run_mode(int R2, int MT, int WN, int nst, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
+    (void)K;
+    if (R2 == 2) cgs_tiles<16, 2, MODE>(MT, WN, nst, grid, s, a);
+    else if (R2 == 4) cgs_tiles<16, 4, MODE>(MT, WN, nst, grid, s, a);
+    else cgs_tiles<16, 0, MODE>(MT, WN, nst, grid, s, a);
 }
 template <int MODE>
 void cgs_allow_mode() {
-    cgs_allow_tiles<16, 2, MODE>(); cgs_allow_tiles<28, 2, MODE>();
-    cgs_allow_tiles<16, 4, MODE>(); cgs_allow_tiles<28, 4, MODE>();
-    cgs_allow_tiles<16, 0, MODE>(); cgs_allow_tiles<28, 0, MODE>();
+    cgs_allow_tiles<16, 2, MODE>();
+    cgs_allow_tiles<16, 4, MODE>();
+    cgs_allow_tiles<16, 0, MODE>();
 }
 
 }  // namespace
 
-void cgs_run(int mode, int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
-    if (mode == CG_UPX) cgs_run_mode<CG_UPX>(R2, MT, WN, K, grid, s, a);
-    else if (mode == CG_UPY) cgs_run_mode<CG_UPY>(R2, MT, WN, K, grid, s, a);
-    else cgs_run_mode<CG_DOWN>(R2, MT, WN, K, grid, s, a);
+void cgs_run(int mode, int R2, int MT, int WN, int nst, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
+    if (mode == CG_UPX) cgs_run_mode<CG_UPX>(R2, MT, WN, nst, K, grid, s, a);
+    else if (mode == CG_UPY) cgs_run_mode<CG_UPY>(R2, MT, WN, nst, K, grid, s, a);
+    else cgs_run_mode<CG_DOWN>(R2, MT, WN, nst, K, grid, s, a);
 }
 void cgs_allow() {
     cgs_allow_mode<CG_UPX>();

@@ -49,12 +49,69 @@ __device__ __forceinline__ void cgs_fetch1(const CgemmSymArgs& s, int m, int pos
     }
 }
 
-template <int MT, int WN, int BK, int WM = 1>
-constexpr size_t cgemm_sym_smem_bytes() {
-    return 4 * (size_t)BK * ((8 * MT * WM + 2) + (8 * WN + 2)) * sizeof(double2);
+// epilogue: half row rr -> rows oA[rr] (y_A) and oB[rr] (y_B)
+template <int R2T, int MODE, int MT>
+__device__ __forceinline__ void cgs_epilogue(const CgemmSymArgs& s, int m, int row0, int col0, int mrow0, int warp,
+                                             int g, int t4, const double (&acc)[2][MT][4]) {
+    const CgemmArgs& a = s.g;
+    const int R2 = R2T ? R2T : a.R2;
+    const int hr = a.rows, ncols = a.nodes * R2;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const int rr = row0 + mrow0 + i * 8 + g;
+        if (rr >= hr) continue;
+        const int ra = s.oA[rr], rbw = s.oB[rr];
+        const double so = 0.5 * s.os[rr];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int col = col0 + warp * 8 + 2 * t4 + j;
+            if (col >= ncols) continue;
+            const int node = col / R2, r2 = col % R2;
+            const double pr = acc[0][i][j], pi = acc[0][i][2 + j], dr = acc[1][i][j], di = acc[1][i][2 + j];
+            double2 yA = make_double2(0.5 * (pr + dr), 0.5 * (pi + di));
+            double2 yB = make_double2(so * (pr - dr), so * (pi - di));
+            if (MODE == CG_UPX) {
+                double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
+                dst[((size_t)node * s.n3 + ra) * R2 + r2] = yA;
+                dst[((size_t)node * s.n3 + rbw) * R2 + r2] = yB;
+            } else if (MODE == CG_UPY) {
+                const int base = cg_child_base(a, node);
+                const double2 ea = a.add[((size_t)m * a.add_ps + base + a.ai0[ra]) * R2 + r2];
+                const double2 eb = a.add[((size_t)m * a.add_ps + base + a.ai0[rbw]) * R2 + r2];
+                double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
+                dst[((size_t)node * s.next + ra) * R2 + r2] = make_double2(yA.x + ea.x, yA.y + ea.y);
+                dst[((size_t)node * s.next + rbw) * R2 + r2] = make_double2(yB.x + eb.x, yB.y + eb.y);
+            } else {   // DOWN: u3 = y + w3, scattered to the edge array
+                const double2* w3 = a.add + (size_t)m * a.add_ps * R2;
+                const double2 wa = w3[((size_t)node * s.n3 + ra) * R2 + r2];
+                const double2 wb = w3[((size_t)node * s.n3 + rbw) * R2 + r2];
+                a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + ra]) * R2 + r2] =
+                    make_double2(yA.x + wa.x, yA.y + wa.y);
+                a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + rbw]) * R2 + r2] =
+                    make_double2(yB.x + wb.x, yB.y + wb.y);
+            }
+        }
+    }
 }
 
-template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1>
+template <int MT, int WN, int BK, int WM = 1, int NST = 2>
+constexpr size_t cgemm_sym_smem_bytes() {
+    return (size_t)NST * 2 * BK * ((8 * MT * WM + 2) + (8 * WN + 2)) * sizeof(double2);
+}
+
+// gathered source address of x at full input position pos (UP-Y, DOWN: one 16-byte value)
+template <int R2T, int MODE>
+__device__ __forceinline__ const double2* cgs_src(const CgemmSymArgs& s, int m, int pos, int node, int r2) {
+    const CgemmArgs& a = s.g;
+    const int R2 = R2T ? R2T : a.R2;
+    if (MODE == CG_UPY) return a.src + (size_t)m * a.src_ps * R2 + ((size_t)node * s.n3 + pos) * R2 + r2;
+    return a.src + ((size_t)m * a.src_ps + a.bi0[(size_t)node * s.next + pos]) * R2 + r2;   // DOWN
+}
+
+// NST = 2: B+- formed through registers.  NST = 3 (UP-Y / DOWN): both halves of A
+// and the raw x_A, x_B tiles by cp.async into a 3-stage ring; B+- formed in the
+// compute loop (b+- = x_A +- s x_B).
+template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int NST = 2>
 __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
     const CgemmArgs& a = s.g;
     constexpr int BM = 8 * MT * WM, BN = 8 * WN, NT = 32 * WN * WM;
@@ -76,6 +133,81 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
     const double2* Ap = a.A + (size_t)m * 2 * hr * hk;   // M+
     const double2* Am = Ap + (size_t)hr * hk;            // M-
 
+    if constexpr (NST >= 3 && (MODE == CG_UPY || MODE == CG_DOWN)) {
+        // ring of NST stages: [stage][half] A tiles, then [stage][A|B] raw x tiles
+        auto AsN = [&](int st, int hf) { return sm + (st * 2 + hf) * BK * LDA; };
+        auto XsN = [&](int st, int ab) { return sm + NST * 2 * BK * LDA + (st * 2 + ab) * BK * LDB; };
+        auto issue = [&](int st, int k0) {
+            for (int e = tid; e < 2 * BK * BM; e += NT) {
+                const int hf = e / (BK * BM), ee = e % (BK * BM);
+                const int kk = ee / BM, r = ee % BM;
+                const int row = row0 + r, k = k0 + kk;
+                double2* base = AsN(st, hf);
+                const double2* M = hf ? Am : Ap;
+                if (row < hr && k < hk) cp_async16(base + kk * LDA + r, M + (size_t)k * hr + row);
+                else base[kk * LDA + r] = make_double2(0.0, 0.0);
+            }
+            for (int e = tid; e < 2 * BK * BN; e += NT) {
+                const int ab = e / (BK * BN), ee = e % (BK * BN);
+                const int kk = ee / BN, c = ee % BN;
+                const int k = k0 + kk, col = col0 + c;
+                double2* base = XsN(st, ab);
+                if (k < hk && col < ncols)
+                    cp_async16(base + kk * LDB + c,
+                               cgs_src<R2T, MODE>(s, m, ab ? s.iB[k] : s.iA[k], col / R2, col % R2));
+                else base[kk * LDB + c] = make_double2(0.0, 0.0);
+            }
+            cp_async_commit();
+        };
+        double acc3[2][MT][4];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int i = 0; i < MT; ++i) acc3[hf][i][0] = acc3[hf][i][1] = acc3[hf][i][2] = acc3[hf][i][3] = 0.0;
+        const int nch = (hk + BK - 1) / BK;
+#pragma unroll
+        for (int st = 0; st < NST - 1; ++st) {
+            if (st < nch) issue(st, st * BK);
+            else cp_async_commit();
+        }
+        for (int ch = 0; ch < nch; ++ch) {
+            cp_async_wait_group<NST - 2>();
+            __syncthreads();
+            const int nx = ch + NST - 1;
+            if (nx < nch) issue(nx % NST, nx * BK);
+            else cp_async_commit();
+            const int st = ch % NST;
+            const double2* XA = XsN(st, 0);
+            const double2* XB = XsN(st, 1);
+#pragma unroll
+            for (int ks = 0; ks < BK / 4; ++ks) {
+                const int kk = ks * 4 + t4;
+                const int k = ch * BK + kk;
+                const double sg = k < hk ? __ldg(s.is + k) : 0.0;
+                const double2 xa = XA[kk * LDB + warp * 8 + g], xb = XB[kk * LDB + warp * 8 + g];
+                const double2 bp = make_double2(xa.x + sg * xb.x, xa.y + sg * xb.y);
+                const double2 bm = make_double2(xa.x - sg * xb.x, xa.y - sg * xb.y);
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const double2* Ab = AsN(st, hf);
+                    const double2 b = hf ? bm : bp;
+                    double2 av[MT];
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + mrow0 + i * 8 + g];
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][0], acc3[hf][i][1], av[i].x, b.x);
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][2], acc3[hf][i][3], av[i].x, b.y);
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][0], acc3[hf][i][1], av[i].y, -b.y);
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][2], acc3[hf][i][3], av[i].y, b.x);
+                }
+            }
+        }
+        cgs_epilogue<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, acc3);
+        return;
+    }
     // buffers: [buf][half] A tiles, then [buf][half] B tiles
     auto As = [&](int buf, int hf) { return sm + (buf * 2 + hf) * BK * LDA; };
     auto Bs = [&](int buf, int hf) { return sm + 4 * BK * LDA + (buf * 2 + hf) * BK * LDB; };
@@ -171,43 +303,7 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
         }
         __syncthreads();
     }
-    // epilogue: half row rr -> rows oA[rr] (y_A) and oB[rr] (y_B)
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-        const int rr = row0 + mrow0 + i * 8 + g;
-        if (rr >= hr) continue;
-        const int ra = s.oA[rr], rbw = s.oB[rr];
-        const double so = 0.5 * s.os[rr];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int col = col0 + warp * 8 + 2 * t4 + j;
-            if (col >= ncols) continue;
-            const int node = col / R2, r2 = col % R2;
-            const double pr = acc[0][i][j], pi = acc[0][i][2 + j], dr = acc[1][i][j], di = acc[1][i][2 + j];
-            double2 yA = make_double2(0.5 * (pr + dr), 0.5 * (pi + di));
-            double2 yB = make_double2(so * (pr - dr), so * (pi - di));
-            if (MODE == CG_UPX) {
-                double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
-                dst[((size_t)node * s.n3 + ra) * R2 + r2] = yA;
-                dst[((size_t)node * s.n3 + rbw) * R2 + r2] = yB;
-            } else if (MODE == CG_UPY) {
-                const int base = cg_child_base(a, node);
-                const double2 ea = a.add[((size_t)m * a.add_ps + base + a.ai0[ra]) * R2 + r2];
-                const double2 eb = a.add[((size_t)m * a.add_ps + base + a.ai0[rbw]) * R2 + r2];
-                double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
-                dst[((size_t)node * s.next + ra) * R2 + r2] = make_double2(yA.x + ea.x, yA.y + ea.y);
-                dst[((size_t)node * s.next + rbw) * R2 + r2] = make_double2(yB.x + eb.x, yB.y + eb.y);
-            } else {   // DOWN: u3 = y + w3, scattered to the edge array
-                const double2* w3 = a.add + (size_t)m * a.add_ps * R2;
-                const double2 wa = w3[((size_t)node * s.n3 + ra) * R2 + r2];
-                const double2 wb = w3[((size_t)node * s.n3 + rbw) * R2 + r2];
-                a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + ra]) * R2 + r2] =
-                    make_double2(yA.x + wa.x, yA.y + wa.y);
-                a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + rbw]) * R2 + r2] =
-                    make_double2(yB.x + wb.x, yB.y + wb.y);
-            }
-        }
-    }
+    cgs_epilogue<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, acc);
 }
 
 }  // namespace dev

@@ -33,7 +33,7 @@
 namespace rexp {
 namespace dev {
 
-void cgs_run(int mode, int R2, int MT, int WN, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a);
+void cgs_run(int mode, int R2, int MT, int WN, int nst, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a);
 void cgs_allow();
 
 __device__ __forceinline__ void cfma(double2& acc, const double2 a, const double2 b) {
@@ -1631,7 +1631,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
         a.nrowblk = (a.rows + bm - 1) / bm;
         const int ncb = (L.nodes * R2 + 8 * cfg.WN - 1) / (8 * cfg.WN);
         tbeg(s);
-        cgs_run(mode, R2, cfg.MT, cfg.WN, a.K, dim3(a.nrowblk * ncb, pc), s, sa);
+        cgs_run(mode, R2, cfg.MT, cfg.WN, cfg.minb == 3 ? 3 : 2, a.K, dim3(a.nrowblk * ncb, pc), s, sa);
         tend(cls, s);
         return REXP_OK;
     }
@@ -1759,8 +1759,8 @@ int DeviceStore::tune_stages(bool measure) {
         const char* st = std::getenv("REXP_GEMM_STAGES");
         if (st && std::string(st) == "3") {
             for (size_t li = 0; li < nl; ++li) {
-                if (t_upy[li].kind == 0) t_upy[li].minb = 3;
-                if (t_down[li].kind == 0) t_down[li].minb = 3;
+                if (t_upy[li].kind == 0 || t_upy[li].kind == 3) t_upy[li].minb = 3;
+                if (t_down[li].kind == 0 || t_down[li].kind == 3) t_down[li].minb = 3;
             }
             return REXP_OK;
         }
@@ -1809,12 +1809,15 @@ int DeviceStore::tune_stages(bool measure) {
                         c.kind = 2; c.rb = rb; c.nb = nb;
                         cands.push_back(c);
                     }
-            for (int mt : {2, 4})
-                for (int wn : {2, 4, 8}) {
-                    StageCfg c;
-                    c.kind = 3; c.MT = mt; c.WN = wn;
-                    cands.push_back(c);
-                }
+            for (int nst : {2, 3}) {
+                if (nst == 3 && kind == 0) continue;   // 3-stage ring: plain-gather modes (UP-Y, DOWN)
+                for (int mt : {2, 4})
+                    for (int wn : {2, 4, 8}) {
+                        StageCfg c;
+                        c.kind = 3; c.MT = mt; c.WN = wn; c.minb = nst == 3 ? 3 : 1;
+                        cands.push_back(c);
+                    }
+            }
             float bt = time_cfg(kind, li, best);
             for (const StageCfg& c : cands) {
                 const float t = time_cfg(kind, li, c);
@@ -1862,7 +1865,9 @@ int DeviceStore::tune_stages(bool measure) {
 
 std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
-        if (c.kind == 3) return "symgemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN);
+        if (c.kind == 3)
+            return "symgemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
+                   (c.minb == 3 ? "s3" : "");
         return c.kind == 2 ? "sym" + std::to_string(c.rb) + (c.nb ? "n" + std::to_string(c.nb) : "")
                            : c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +

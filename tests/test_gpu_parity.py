@@ -152,14 +152,20 @@ def test_config0_three_stage_gemm(c0, nrhs, monkeypatch):
     h.close()
 
 
-def test_config0_symmetric_pair_gemm_many_rhs(c0):
+@pytest.mark.parametrize("stages", ["tuned", "3"])
+def test_config0_symmetric_pair_gemm_many_rhs(c0, stages, monkeypatch):
     """nrhs = 8 (R2 = 16): every merge level above the first runs as the
-    symmetric-pair DMMA GEMM (k_cgemm_sym) or GEMV; parity per RHS."""
+    symmetric-pair DMMA GEMM (k_cgemm_sym) or GEMV; "3" forces the 3-stage
+    cp.async variant on its up-Y / down stages; parity per RHS."""
     cfg, m, op, u0 = c0
     Lam = cfg["Lambda_tau"] / cfg["tau"]
+    if stages == "3":
+        monkeypatch.setenv("REXP_GEMM_STAGES", "3")
     U = np.stack([rsw_initial_state(m.x, m.y, cfg["seed"] + 10 * k) for k in range(8)])
     h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], nrhs=8)
     assert "symgemm" in h.stage_report
+    if stages == "3":
+        assert "s3" in h.stage_report
     got = _gpu_apply(h, U, 2)
     errs = [rel_l2(got[k], op.evolve(U[k], 2)) for k in range(8)]
     print(f"symmetric-pair GEMM nrhs 8: max rel L2 {max(errs):.3e}")
