@@ -82,9 +82,12 @@ void cg_allow_tiles() {
 
 // BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16;
 // R2 = 2, 4 compiled in, anything else at run time
+// MINB bit 16: use BK = 16 even when K is a multiple of 28 (smaller shared-memory
+// footprint, more resident CTAs; an autotuner candidate)
 void run(int R2, int MT, int WN, int MINB, int K, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     constexpr int M = CG_MODE;
-    const bool b28 = (K % 28) == 0;
+    const bool b28 = (K % 28) == 0 && !(MINB & 16);
+    MINB &= 15;
     if (R2 == 2) {
         if (b28) cg_tiles<28, 2, M>(MT, WN, MINB, grid, s, a);
         else cg_tiles<16, 2, M>(MT, WN, MINB, grid, s, a);

@@ -1825,15 +1825,21 @@ int DeviceStore::tune_stages(bool measure) {
             }
             return;
         }
-        // minb: 1 = default, 4 = register-capped, 3 = 3-stage cp.async ring (UP-Y / DOWN)
-        for (int minb : {1, 4, 3}) {
-            if (minb == 3 && kind != 1 && kind != 2) continue;
-            for (int mt : {2, 4})
-                for (int wn : {2, 4, 8}) {
-                    StageCfg c;
-                    c.kind = 0; c.MT = mt; c.WN = wn; c.minb = minb;
-                    cands.push_back(c);
-                }
+        // minb: 1 = default, 4 = register-capped, 3 = 3-stage cp.async ring (UP-Y / DOWN);
+        // + 16: BK = 16 where K is a multiple of 28 (smaller footprint)
+        const Level& Lv = levels[li];
+        const int Kst = kind == 2 ? Lv.next : kind == 3 ? ns : Lv.n3;
+        for (int bk16 : {0, 16}) {
+            if (bk16 && Kst % 28 != 0) continue;
+            for (int minb : {1, 4, 3}) {
+                if (minb == 3 && kind != 1 && kind != 2) continue;
+                for (int mt : {2, 4})
+                    for (int wn : {2, 4, 8}) {
+                        StageCfg c;
+                        c.kind = 0; c.MT = mt; c.WN = wn; c.minb = minb | bk16;
+                        cands.push_back(c);
+                    }
+            }
         }
         if (gemv_ok) {
             for (int rb : {32, 64, 128, 256}) {
@@ -1871,7 +1877,7 @@ std::string DeviceStore::stage_report() const {
         return c.kind == 2 ? "sym" + std::to_string(c.rb) + (c.nb ? "n" + std::to_string(c.nb) : "")
                            : c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
-                                 (c.minb == 4 ? "r" : c.minb == 3 ? "s3" : "");
+                                 ((c.minb & 15) == 4 ? "r" : (c.minb & 15) == 3 ? "s3" : "") + (c.minb & 16 ? "k16" : "");
     };
     std::string s = tuned ? "tuned:" : "default:";
     for (size_t li = 0; li < levels.size(); ++li)
