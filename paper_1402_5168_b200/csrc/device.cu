@@ -1766,7 +1766,9 @@ int DeviceStore::tune_stages(bool measure) {
         }
     }
     const char* env = std::getenv("REXP_AUTOTUNE");
-    if (!measure || (env && std::string(env) == "0") || !shared) return REXP_OK;
+    if (!measure || (env && std::string(env) == "0")) return REXP_OK;
+    // per-node store: only the GEMV shapes are candidates (no shared operator to
+    // apply to many nodes at once)
 
     const int pc = chunk;
     cudaStream_t s = nullptr;
@@ -1830,6 +1832,7 @@ int DeviceStore::tune_stages(bool measure) {
         const Level& Lv = levels[li];
         const int Kst = kind == 2 ? Lv.next : kind == 3 ? ns : Lv.n3;
         for (int bk16 : {0, 16}) {
+            if (!shared) break;
             if (bk16 && Kst % 28 != 0) continue;
             for (int minb : {1, 4, 3}) {
                 if (minb == 3 && kind != 1 && kind != 2) continue;
