@@ -190,11 +190,27 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
         cp_async_commit();
     };
     BRaw braw[BPT];
+    // B element of thread slot e: (kk, c).  With compile-time R2 the merge modes map
+    // consecutive e to (real part, k, node) so consecutive threads read consecutive
+    // addresses of the node-major gathered vectors
+    constexpr bool kBmap = R2T != 0 && MODE != CG_LEAF_UP && MODE != CG_LEAF_DOWN && (BN % (R2T ? R2T : 1)) == 0;
+    auto bslot = [&](int e, int& kk, int& c) {
+        if (kBmap) {
+            constexpr int R = R2T ? R2T : 1;
+            const int r2 = e % R, t2 = e / R;
+            kk = t2 % BK;
+            c = (t2 / BK) * R + r2;
+        } else {
+            kk = e / BN;
+            c = e % BN;
+        }
+    };
     auto fetch_B = [&](int k0) {
 #pragma unroll
         for (int u = 0; u < BPT; ++u) {
             const int e = tid + u * NT;
-            const int kk = e / BN, c = e % BN;
+            int kk, c;
+            bslot(e, kk, c);
             const int k = k0 + kk, col = col0 + c;
             braw[u].v[0] = braw[u].v[1] = braw[u].v[2] = braw[u].v[3] = 0.0;
             if (e < BK * BN && k < a.K && col < ncols) cg_fetch<R2T, MODE>(a, m, k, col, braw[u]);
@@ -205,7 +221,11 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
 #pragma unroll
         for (int u = 0; u < BPT; ++u) {
             const int e = tid + u * NT;
-            if (e < BK * BN) base[(e / BN) * LDB + (e % BN)] = cg_form<MODE>(braw[u], cf);
+            if (e < BK * BN) {
+                int kk, c;
+                bslot(e, kk, c);
+                base[kk * LDB + c] = cg_form<MODE>(braw[u], cf);
+            }
         }
     };
 
@@ -217,7 +237,9 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
 
     // additive epilogue terms (LEAF_DOWN: w, DOWN: w3, UPY: child h[ext]) fetched
     // before the K loop so their latency overlaps the products
-    constexpr bool kAdd = (MODE == CG_LEAF_DOWN || MODE == CG_DOWN || MODE == CG_UPY);
+    // UP-Y with compile-time R2 uses the staged, coalesced epilogue below instead
+    constexpr bool kStagedUPY = (MODE == CG_UPY && R2T != 0);
+    constexpr bool kAdd = (MODE == CG_LEAF_DOWN || MODE == CG_DOWN || (MODE == CG_UPY && !kStagedUPY));
     double2 addv[kAdd ? MT : 1][kAdd ? NTW : 1][2];
     if (kAdd) {
 #pragma unroll
@@ -324,6 +346,36 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
             }
             __syncthreads();
         }
+    }
+    if constexpr (kStagedUPY) {
+        // staged epilogue: C tile -> shared memory [local col][row], then each node's
+        // rows x R2 run (contiguous in h) written and its child term h[ext] read
+        // with consecutive threads on consecutive addresses
+        constexpr int LDC = BM + 1;
+        double2* Cs = sm;   // BN x LDC, reuses the A/B buffers
+        __syncthreads();    // every warp is done reading them (the 3-stage loop ends without a barrier)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    Cs[((warp * NTW + n) * 8 + 2 * t4 + j) * LDC + mrow0 + i * 8 + g] =
+                        make_double2(acc[i][n][j], acc[i][n][2 + j]);
+        __syncthreads();
+        constexpr int NPT = BN / R2T;                  // nodes per tile
+        double2* dst = a.dst + (size_t)m * a.dst_ps * R2T;
+        const double2* add = a.add + (size_t)m * a.add_ps * R2T;
+        for (int e = tid; e < NPT * BM * R2T; e += NT) {
+            const int r2 = e % R2T, rl = (e / R2T) % BM, nl = e / (R2T * BM);
+            const int row = row0 + rl, col = col0 + nl * R2T + r2;
+            if (row >= a.rows || col >= ncols) continue;
+            const int node = col / R2T;
+            const double2 ad = add[(size_t)(cg_child_base(a, node) + a.ai0[row]) * R2T + r2];
+            const double2 v = Cs[(nl * R2T + r2) * LDC + rl];
+            dst[((size_t)node * a.rows + row) * R2T + r2] = make_double2(v.x + ad.x, v.y + ad.y);
+        }
+        return;
     }
     // epilogue: C[g][2 t4 + j] of each tile
 #pragma unroll
