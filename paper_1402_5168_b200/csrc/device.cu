@@ -488,40 +488,44 @@ __global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a, SymPairs sp) {
         const double2* Mm = Mp + (size_t)hr * hc;
         const int CS = a.CS;
         int c = cs;
-        // software pipelined: the next 4 columns of both matrices (8 loads) are in
-        // flight while the current 4 are used
-        if (c + 3 * CS < hc) {
-            double2 vp[4], vm[4], np[4], nm[4];
+        // ping-pong over two register batches of 4 columns of both matrices: a
+        // batch is refilled right after it is consumed, so 8 loads stay in flight
+        // while the other batch computes (no register copies waiting on loads)
+        auto ldb = [&](double2 (&bp)[4], double2 (&bm)[4], int cc) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                vp[u] = ldg2(Mp + (size_t)(c + u * CS) * hr);
-                vm[u] = ldg2(Mm + (size_t)(c + u * CS) * hr);
+                bp[u] = ldg2(Mp + (size_t)(cc + u * CS) * hr);
+                bm[u] = ldg2(Mm + (size_t)(cc + u * CS) * hr);
             }
-            for (;;) {
-                const int cn = c + 4 * CS;
-                const bool more = cn + 3 * CS < hc;
-                if (more) {
+        };
+        auto use = [&](const double2 (&bp)[4], const double2 (&bm)[4], int cc) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        np[u] = ldg2(Mp + (size_t)(cn + u * CS) * hr);
-                        nm[u] = ldg2(Mm + (size_t)(cn + u * CS) * hr);
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int r = 0; r < R2; ++r) {
+                        cfma(ap[nb][r], bp[u], xs[((nb * 2 + 0) * hc + cc + u * CS) * R2 + r]);
+                        cfma(am[nb][r], bm[u], xs[((nb * 2 + 1) * hc + cc + u * CS) * R2 + r]);
                     }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                        for (int r = 0; r < R2; ++r) {
-                            cfma(ap[nb][r], vp[u], xs[((nb * 2 + 0) * hc + c + u * CS) * R2 + r]);
-                            cfma(am[nb][r], vm[u], xs[((nb * 2 + 1) * hc + c + u * CS) * R2 + r]);
-                        }
-                c = cn;
-                if (!more) break;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    vp[u] = np[u];
-                    vm[u] = nm[u];
+        };
+        if (c + 7 * CS < hc) {
+            double2 p0[4], m0[4], p1[4], m1[4];
+            ldb(p0, m0, c);
+            ldb(p1, m1, c + 4 * CS);
+            for (;;) {
+                use(p0, m0, c);
+                const bool more0 = c + 11 * CS < hc;         // batch c + 8 CS fully in range
+                if (more0) ldb(p0, m0, c + 8 * CS);
+                use(p1, m1, c + 4 * CS);
+                c += 8 * CS;
+                if (!more0) break;
+                if (c + 7 * CS < hc) {
+                    ldb(p1, m1, c + 4 * CS);
+                } else {                                     // only batch p0 left in range
+                    use(p0, m0, c);
+                    c += 4 * CS;
+                    break;
                 }
             }
         }
