@@ -141,8 +141,14 @@ __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int
 }
 
 template <int MT, int WN, int BK, int NTW = 1, int WM = 1, int NST = 2>
-constexpr size_t cgemm_smem_bytes() {
+__host__ __device__ constexpr size_t cgemm_smem_bytes() {
     return (size_t)NST * BK * ((8 * MT * WM + 2) + (8 * WN * NTW + 2)) * sizeof(double2);
+}
+// UP-Y (compile-time R2): the additive child term of the tile is staged too
+template <int MT, int WN, int BK, int NTW = 1, int WM = 1, int NST = 2, int MODE = 0>
+__host__ __device__ constexpr size_t cgemm_smem_total() {
+    return cgemm_smem_bytes<MT, WN, BK, NTW, WM, NST>() +
+           (MODE == CG_UPY ? (size_t)(8 * MT * WM) * (8 * WN * NTW) * sizeof(double2) : 0);
 }
 
 // MT m-tiles and NTW n-tiles per warp; WN warps side by side in n, WM in m.
@@ -263,6 +269,19 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
                 }
     }
 
+    // UP-Y staged epilogue: the tile's additive child term h[ext] -> shared memory by
+    // cp.async now (it lands with the first operand chunk), [node][row][R2] order
+    double2* Adds = sm + cgemm_smem_bytes<MT, WN, BK, NTW, WM, NST>() / sizeof(double2);
+    if constexpr (kStagedUPY) {
+        constexpr int R = R2T ? R2T : 1;
+        for (int e = tid; e < (BN / R) * BM * R; e += NT) {
+            const int r2 = e % R, rl = (e / R) % BM, nl = e / (R * BM);
+            const int row = row0 + rl, col = col0 + nl * R + r2;
+            if (row < a.rows && col < ncols)
+                cp_async16(Adds + e, a.add + ((size_t)m * a.add_ps + cg_child_base(a, col / R) + a.ai0[row]) * R + r2);
+        }
+        cp_async_commit();
+    }
     const int nchunks = (a.K + BK - 1) / BK;
     auto compute = [&](const double2* Ab, const double2* Bb) {
 #pragma unroll
@@ -353,6 +372,7 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
         // with consecutive threads on consecutive addresses
         constexpr int LDC = BM + 1;
         double2* Cs = sm;   // BN x LDC, reuses the A/B buffers
+        cp_async_wait_all();
         __syncthreads();    // every warp is done reading them (the 3-stage loop ends without a barrier)
 #pragma unroll
         for (int i = 0; i < MT; ++i)
@@ -365,13 +385,12 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
         __syncthreads();
         constexpr int NPT = BN / R2T;                  // nodes per tile
         double2* dst = a.dst + (size_t)m * a.dst_ps * R2T;
-        const double2* add = a.add + (size_t)m * a.add_ps * R2T;
         for (int e = tid; e < NPT * BM * R2T; e += NT) {
             const int r2 = e % R2T, rl = (e / R2T) % BM, nl = e / (R2T * BM);
             const int row = row0 + rl, col = col0 + nl * R2T + r2;
             if (row >= a.rows || col >= ncols) continue;
             const int node = col / R2T;
-            const double2 ad = add[(size_t)(cg_child_base(a, node) + a.ai0[row]) * R2T + r2];
+            const double2 ad = Adds[e];
             const double2 v = Cs[(nl * R2T + r2) * LDC + rl];
             dst[((size_t)node * a.rows + row) * R2T + r2] = make_double2(v.x + ad.x, v.y + ad.y);
         }

@@ -12,7 +12,7 @@ namespace {
 template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int MINB = 1, int NST = 2>
 void cg_launch(dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     k_cgemm<MT, WN, BK, R2T, MODE, 1, MINB, WM, NST>
-        <<<grid, 32 * WN * WM, cgemm_smem_bytes<MT, WN, BK, 1, WM, NST>(), s>>>(a);
+        <<<grid, 32 * WN * WM, cgemm_smem_total<MT, WN, BK, 1, WM, NST, (R2T != 0 ? MODE : 0)>(), s>>>(a);
 }
 // leaf tiles: MT in {4, 5}, WN = 8; merge tiles: MT in {2, 4} with
 //   WN = 8, WM = 1 | WN = 4, WM = 2 | WN = 2, WM = 4
