@@ -595,6 +595,36 @@ __global__ void __launch_bounds__(256) k_gemv_sym(GemvArgs a, SymPairs sp) {
 }
 
 // --------------------------------------------------------------------------
+// k_upx_diag: first merge level of the spectral shared store.  Its interface is
+// one q-node segment between two leaves, and in the spectral edge basis the
+// leaf's side-to-side DtN blocks are diagonal (the tangential modes decouple on
+// a Kronecker-sum leaf), so X = -(T^a_33 + T^b_33)^{-1} is diagonal
+// (tests/test_setup_host.py): w3[t] = X[t][t] (h^a_3[t] + h^b_3[t]).
+// --------------------------------------------------------------------------
+struct UpxDiagArgs {
+    const double2* X;       // [pc][n3 x n3] column-major (diagonal used)
+    const double2* h;       // child h (leaves), [pc][hps][R2]
+    long long hps;
+    const int *ia3, *ib3;   // node-0 rows (affine in the node)
+    double2* w3;            // [pc][nodes][n3][R2]
+    int nodes, n3, R2, nbx, xdir, nchild;
+};
+
+__global__ void k_upx_diag(UpxDiagArgs a) {
+    const long long per = (long long)a.nodes * a.n3 * a.R2;
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= per) return;
+    const int m = blockIdx.y;
+    const int r2 = (int)(t % a.R2), k = (int)((t / a.R2) % a.n3), node = (int)(t / ((long long)a.R2 * a.n3));
+    const int base = (a.xdir ? 2 * node : node + (node / a.nbx) * a.nbx) * a.nchild;
+    const double2* hm = a.h + (size_t)m * a.hps * a.R2;
+    const double2 u = hm[(size_t)(base + a.ia3[k]) * a.R2 + r2], v = hm[(size_t)(base + a.ib3[k]) * a.R2 + r2];
+    const double2 x = __ldg(a.X + (size_t)m * a.n3 * a.n3 + (size_t)k * (a.n3 + 1));
+    const double sx = u.x + v.x, sy = u.y + v.y;
+    a.w3[(size_t)m * per + t] = make_double2(x.x * sx - x.y * sy, x.x * sy + x.y * sx);
+}
+
+// --------------------------------------------------------------------------
 // k_root_fourier: periodic closure of the shared store in Fourier space.
 // The seam operator is block circulant in the element index e along x
 // (setup_host.cpp): s = X (h^a_3 + h^b_3) is applied as
@@ -1198,6 +1228,9 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         Level& D = levels[li];
         D.nodes = L.nodes; D.n3 = L.n3; D.next = L.next; D.nchild = L.nchild; D.child_nodes = L.child_nodes;
         D.nbx = L.nbx; D.dir = L.dir;
+        // first level of the spectral path with a one-segment interface: X is diagonal
+        // in the edge basis (k_upx_diag)
+        D.xdiag = fdm && li == 0 && L.n3 == T.q && std::getenv("REXP_NO_XDIAG") == nullptr;
         const size_t st = shared ? 1 : static_cast<size_t>(L.nodes);
         // top levels of the spectral shared store (few nodes: GEMV stages) keep only
         // the symmetric half pair [M+ | M-] of each operator (k_gemv_sym)
@@ -1603,6 +1636,17 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     const double2* hc = d_h[li % 2];
     double2* hp = d_h[(li + 1) % 2];
     const int cls = kind == 2 ? T_MERGE_DOWN : T_MERGE_UP;
+    if (kind == 0 && L.xdiag) {
+        UpxDiagArgs u{};
+        u.X = L.X + static_cast<size_t>(m0) * L.ppX; u.h = hc; u.hps = hstride; u.ia3 = L.ia3; u.ib3 = L.ib3;
+        u.w3 = L.w3; u.nodes = L.nodes; u.n3 = L.n3; u.R2 = R2; u.nbx = L.nbx; u.xdir = L.dir == 0 ? 1 : 0;
+        u.nchild = L.nchild;
+        const long long per = static_cast<long long>(L.nodes) * L.n3 * R2;
+        tbeg(s);
+        k_upx_diag<<<dim3(static_cast<unsigned>((per + 255) / 256), pc), 256, 0, s>>>(u);
+        tend(cls, s);
+        return REXP_OK;
+    }
     if (L.sym && cfg.kind == 3) {
         CgemmSymArgs sa{};
         CgemmArgs& a = sa.g;
@@ -1862,7 +1906,7 @@ int DeviceStore::tune_stages(bool measure) {
         }
     };
     for (size_t li = 0; li < nl; ++li) {
-        tune(0, li, t_upx[li]);
+        if (!levels[li].xdiag) tune(0, li, t_upx[li]);
         tune(1, li, t_upy[li]);
         tune(2, li, t_down[li]);
     }
@@ -1888,7 +1932,8 @@ std::string DeviceStore::stage_report() const {
     };
     std::string s = tuned ? "tuned:" : "default:";
     for (size_t li = 0; li < levels.size(); ++li)
-        s += " L" + std::to_string(li + 1) + "[" + one(t_upx[li]) + "," + one(t_upy[li]) + "," + one(t_down[li]) + "]";
+        s += " L" + std::to_string(li + 1) + "[" + (levels[li].xdiag ? std::string("diag") : one(t_upx[li])) + "," +
+             one(t_upy[li]) + "," + one(t_down[li]) + "]";
     s += shared ? std::string(" root[fourier]") : " root[" + one(t_root) + "]";
     return s;
 }

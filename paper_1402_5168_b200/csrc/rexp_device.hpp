@@ -22,6 +22,7 @@ struct StageCfg {
 struct Level {
     int nodes = 0, n3 = 0, next = 0, nchild = 0, child_nodes = 0, nbx = 1, dir = 0;
     bool sym = false;   // stored as the symmetric half pair [M+ | M-] (k_gemv_sym, see sym_pairs)
+    bool xdiag = false; // X diagonal in the edge basis: up-X as k_upx_diag
     int *siA = nullptr, *siB = nullptr, *seA = nullptr, *seB = nullptr;   // interface / boundary pairs
     double *sis = nullptr, *ses = nullptr;                                 // their signs
     std::vector<int> h_iA, h_iB, h_eA, h_eB;

@@ -338,3 +338,23 @@ def test_merge_levels_reflection_symmetry(n):
             assert np.abs(X[np.ix_(pi, pi)] - X).max() <= 1e-12 * np.abs(X).max()
             assert np.abs(Y[np.ix_(pe, pi)] - Y).max() <= 1e-12 * np.abs(Y).max()
             assert np.abs(S[np.ix_(pi, pe)] - S).max() <= 1e-12 * np.abs(S).max()
+
+
+def test_first_level_interface_operator_diagonal_in_edge_basis():
+    """DESIGN.md §2 (k_upx_diag): on a Kronecker-sum leaf the tangential modes of a
+    side decouple, so the first merge level's interface operator X (one q-node
+    segment between two leaves) is diagonal after the edge-basis similarity
+    transform V^-1 X V, K = D2[1..q][1..q] = V diag(l) V^-1."""
+    from paper_1402_5168_b200 import api
+    n, p = 4, 8
+    h = api.setup("rsw", n=n, p=p, tau=0.2, delta=1e-10, Lambda=100.0, f=1.0, device=-1, store="shared")
+    D = Mesh(n, p).D
+    K = (D @ D)[1:p - 1, 1:p - 1]
+    _, V = np.linalg.eig(K)
+    V = np.real(V)
+    Vi = np.linalg.inv(V)
+    n3 = api.export_level_info(h, 1)[2]
+    assert n3 == p - 2
+    for half in (0, h.num_half_poles // 2, h.num_half_poles - 1):
+        Xe = Vi @ api.export_matrix(h, half, 1, 0, 0, n3, n3) @ V
+        assert np.abs(Xe - np.diag(np.diag(Xe))).max() <= 1e-12 * np.abs(Xe).max()
