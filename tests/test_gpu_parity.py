@@ -173,6 +173,26 @@ def test_config0_symmetric_pair_gemm_many_rhs(c0, stages, monkeypatch):
     h.close()
 
 
+def test_config0_long_run_accumulation(c0):
+    """60 steps (graph replay, pole lanes): the error against the oracle must not
+    grow beyond the per-step rounding (no drift from the spectral / pair /
+    Fourier re-expressions).  The plain vector 2-norm is not the discrete energy
+    (L is skew only in a quadrature-weighted inner product), so its change is
+    compared with the oracle's rather than with 1."""
+    cfg, m, op, u0 = c0
+    Lam = cfg["Lambda_tau"] / cfg["tau"]
+    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"])
+    got = _gpu_apply(h, u0, 60)
+    ref = op.evolve(u0, 60)
+    err = rel_l2(got, ref)
+    growth = float(np.linalg.norm(got) / np.linalg.norm(u0))
+    growth_ref = float(np.linalg.norm(ref) / np.linalg.norm(u0))
+    print(f"config0 60 steps rel L2 {err:.3e}, norm ratio {growth:.6f} (oracle {growth_ref:.6f})")
+    assert err <= TOL
+    assert abs(growth - growth_ref) <= 1e-10
+    h.close()
+
+
 def test_edge_cases_zero_state_and_zero_steps(c0):
     cfg, m, op, u0 = c0
     Lam = cfg["Lambda_tau"] / cfg["tau"]
