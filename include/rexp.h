@@ -123,7 +123,11 @@ int rexp_setup(const rexp_problem* prob, double tau, double delta, double Lambda
  * (a cudaStream_t, NULL = legacy default stream).  Otherwise u is a host
  * pointer; the call copies it to the device, steps, copies back and
  * synchronizes `stream` before returning.  Requires a handle that owns all
- * half poles (single-GPU).
+ * half poles (single-GPU).  Each step is replayed from a CUDA graph captured
+ * on first use for this state pointer (recaptured when the pointer changes;
+ * the capture uses a private stream, replay runs on `stream`); the pole lanes
+ * of the spectral path fork from and join back to `stream` inside the step.
+ * Environment REXP_GRAPH=0 launches the kernels directly.
  */
 int rexp_apply(rexp_handle* h, double* u, int32_t nsteps, int32_t u_on_device, void* stream);
 
@@ -162,10 +166,16 @@ int64_t rexp_work_bytes(const rexp_handle* h);
 /* number of kernel launches one step issues (for the bench's gpu_launches) */
 int32_t rexp_launches_per_step(const rexp_handle* h);
 /* leaf solver of the device store: 0 = dense q^2 x q^2 leaf operators,
- * 1 = tensor-product leaf inverse (constant coefficients), -1 = no device store */
+ * 1 = spectral (tensor-product) leaf path of the constant-coefficient store:
+ * leaf solves and interior pole sums in the eigenbasis of D2[1..q][1..q],
+ * edge data in the spectral edge basis, symmetric-pair merge levels and the
+ * Fourier root; -1 = no device store */
 int32_t rexp_leaf_solver(const rexp_handle* h);
 /* kernel chosen for every merge stage (X, Y, down per level) and the closure
- * by the setup-time autotuner, as text (for reports) */
+ * by the setup-time autotuner, as text (for reports): gemmMxN (DMMA GEMM; r =
+ * register-capped, s3 = 3-stage cp.async, k16 = BK 16), gemvRB, symRB[nNB] /
+ * symgemmMxN (symmetric-pair forms), diag (diagonal first-level up-X),
+ * root[fourier] */
 int rexp_stage_report(const rexp_handle* h, char* buf, int32_t len);
 
 /* ---- per-kernel timing (bench) ----
