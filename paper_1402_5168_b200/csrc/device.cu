@@ -1276,7 +1276,8 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     // REXP_LANES overrides, the per-node path uses one lane
     {
         const char* env = std::getenv("REXP_LANES");
-        nlanes = fdm ? (env ? std::atoi(env) : 2) : 1;
+        // (many right-hand sides: every launch already fills the GPU, one lane)
+        nlanes = fdm ? (env ? std::atoi(env) : (R2 >= 16 ? 1 : 2)) : 1;
         nlanes = std::max(1, std::min(nlanes, std::min(nh, 4)));
     }
     {
