@@ -55,6 +55,24 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
+// Complex products on the real DMMA: REXP_CMUL3 = 1 (default) uses the
+// three-multiply form per 8x8 tile,
+//   P1 += Ar Br (acc[0..1]),  P3 += (Ar + Ai)(Br + Bi) (acc[2..3]),  P2 += Ai Bi (q[0..1]),
+// finished after the K loop as Cr = P1 - P2, Ci = P3 - P1 - P2 (cmul3_finish):
+// 3 DMMAs per complex k-step instead of 4 (the merge GEMMs are DMMA-issue bound,
+// profiles/r01_merge_ncu_details.txt: math_pipe_throttle).  0 = four real products.
+#ifndef REXP_CMUL3
+#define REXP_CMUL3 1
+#endif
+__device__ __forceinline__ void cmul3_finish(double* acc, const double* q) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const double p1 = acc[j], p2 = q[j], p3 = acc[2 + j];
+        acc[j] = p1 - p2;
+        acc[2 + j] = p3 - p1 - p2;
+    }
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -236,10 +254,14 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
     };
 
     double acc[MT][NTW][4];
+    double accq[MT][NTW][2];   // REXP_CMUL3: P2 = sum Ai Bi
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int n = 0; n < NTW; ++n) acc[i][n][0] = acc[i][n][1] = acc[i][n][2] = acc[i][n][3] = 0.0;
+        for (int n = 0; n < NTW; ++n) {
+            acc[i][n][0] = acc[i][n][1] = acc[i][n][2] = acc[i][n][3] = 0.0;
+            accq[i][n][0] = accq[i][n][1] = 0.0;
+        }
 
     // additive epilogue terms (LEAF_DOWN: w, DOWN: w3, UPY: child h[ext]) fetched
     // before the K loop so their latency overlaps the products
@@ -293,6 +315,26 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
             double2 av[MT];
 #pragma unroll
             for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + mrow0 + i * 8 + g];   // A[m = g][k = t4]
+#if REXP_CMUL3
+            double bs[NTW], as[MT];
+#pragma unroll
+            for (int n = 0; n < NTW; ++n) bs[n] = b[n].x + b[n].y;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) as[i] = av[i].x + av[i].y;
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[i][n][0], acc[i][n][1], av[i].x, b[n].x);   // P1
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[i][n][2], acc[i][n][3], as[i], bs[n]);       // P3
+#pragma unroll
+            for (int n = 0; n < NTW; ++n)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(accq[i][n][0], accq[i][n][1], av[i].y, b[n].y);  // P2
+            continue;
+#endif
             // four passes so each accumulator is revisited only every 2*MT*NTW DMMAs
 #pragma unroll
             for (int n = 0; n < NTW; ++n)
@@ -366,6 +408,12 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
             __syncthreads();
         }
     }
+#if REXP_CMUL3
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int n = 0; n < NTW; ++n) cmul3_finish(acc[i][n], accq[i][n]);
+#endif
     if constexpr (kStagedUPY) {
         // staged epilogue: C tile -> shared memory [local col][row], then each node's
         // rows x R2 run (contiguous in h) written and its child term h[ext] read

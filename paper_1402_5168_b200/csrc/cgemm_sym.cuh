@@ -159,11 +159,14 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
             }
             cp_async_commit();
         };
-        double acc3[2][MT][4];
+        double acc3[2][MT][4], q3[2][MT][2];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-            for (int i = 0; i < MT; ++i) acc3[hf][i][0] = acc3[hf][i][1] = acc3[hf][i][2] = acc3[hf][i][3] = 0.0;
+            for (int i = 0; i < MT; ++i) {
+                acc3[hf][i][0] = acc3[hf][i][1] = acc3[hf][i][2] = acc3[hf][i][3] = 0.0;
+                q3[hf][i][0] = q3[hf][i][1] = 0.0;
+            }
         const int nch = (hk + BK - 1) / BK;
 #pragma unroll
         for (int st = 0; st < NST - 1; ++st) {
@@ -194,6 +197,16 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                     double2 av[MT];
 #pragma unroll
                     for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + mrow0 + i * 8 + g];
+#if REXP_CMUL3
+                    const double bs = b.x + b.y;
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][0], acc3[hf][i][1], av[i].x, b.x);
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][2], acc3[hf][i][3], av[i].x + av[i].y, bs);
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) dmma884(q3[hf][i][0], q3[hf][i][1], av[i].y, b.y);
+                    continue;
+#endif
 #pragma unroll
                     for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][0], acc3[hf][i][1], av[i].x, b.x);
 #pragma unroll
@@ -205,6 +218,12 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                 }
             }
         }
+#if REXP_CMUL3
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int i = 0; i < MT; ++i) cmul3_finish(acc3[hf][i], q3[hf][i]);
+#endif
         cgs_epilogue<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, acc3);
         return;
     }
@@ -257,11 +276,14 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
         }
     };
 
-    double acc[2][MT][4];
+    double acc[2][MT][4], q2[2][MT][2];
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-        for (int i = 0; i < MT; ++i) acc[hf][i][0] = acc[hf][i][1] = acc[hf][i][2] = acc[hf][i][3] = 0.0;
+        for (int i = 0; i < MT; ++i) {
+            acc[hf][i][0] = acc[hf][i][1] = acc[hf][i][2] = acc[hf][i][3] = 0.0;
+            q2[hf][i][0] = q2[hf][i][1] = 0.0;
+        }
 
     const int nchunks = (hk + BK - 1) / BK;
     issue_A(0, 0);
@@ -287,6 +309,16 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                 double2 av[MT];
 #pragma unroll
                 for (int i = 0; i < MT; ++i) av[i] = Ab[kk * LDA + mrow0 + i * 8 + g];
+#if REXP_CMUL3
+                const double bs = b.x + b.y;
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][0], acc[hf][i][1], av[i].x, b.x);
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][2], acc[hf][i][3], av[i].x + av[i].y, bs);
+#pragma unroll
+                for (int i = 0; i < MT; ++i) dmma884(q2[hf][i][0], q2[hf][i][1], av[i].y, b.y);
+                continue;
+#endif
 #pragma unroll
                 for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][0], acc[hf][i][1], av[i].x, b.x);
 #pragma unroll
@@ -303,6 +335,12 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
         }
         __syncthreads();
     }
+#if REXP_CMUL3
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+        for (int i = 0; i < MT; ++i) cmul3_finish(acc[hf][i], q2[hf][i]);
+#endif
     cgs_epilogue<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, acc);
 }
 
