@@ -333,8 +333,7 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
             for (int n = 0; n < NTW; ++n)
 #pragma unroll
                 for (int i = 0; i < MT; ++i) dmma884(accq[i][n][0], accq[i][n][1], av[i].y, b[n].y);  // P2
-            continue;
-#endif
+#else
             // four passes so each accumulator is revisited only every 2*MT*NTW DMMAs
 #pragma unroll
             for (int n = 0; n < NTW; ++n)
@@ -352,6 +351,7 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
             for (int n = 0; n < NTW; ++n)
 #pragma unroll
                 for (int i = 0; i < MT; ++i) dmma884(acc[i][n][2], acc[i][n][3], av[i].y, b[n].x);    // Ci += Ai Br
+#endif
         }
     };
     if constexpr (NST >= 3 && cg_plain_b<MODE>()) {
@@ -419,6 +419,8 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
         // rows x R2 run (contiguous in h) written and its child term h[ext] read
         // with consecutive threads on consecutive addresses
         constexpr int LDC = BM + 1;
+        static_assert((size_t)BN * LDC * sizeof(double2) <= cgemm_smem_bytes<MT, WN, BK, NTW, WM, NST>(),
+                      "the C tile must fit in the A/B buffers (Adds follows them)");
         double2* Cs = sm;   // BN x LDC, reuses the A/B buffers
         cp_async_wait_all();
         __syncthreads();    // every warp is done reading them (the 3-stage loop ends without a barrier)

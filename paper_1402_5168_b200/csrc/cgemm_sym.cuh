@@ -205,8 +205,7 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                     for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][2], acc3[hf][i][3], av[i].x + av[i].y, bs);
 #pragma unroll
                     for (int i = 0; i < MT; ++i) dmma884(q3[hf][i][0], q3[hf][i][1], av[i].y, b.y);
-                    continue;
-#endif
+#else
 #pragma unroll
                     for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][0], acc3[hf][i][1], av[i].x, b.x);
 #pragma unroll
@@ -215,6 +214,7 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                     for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][0], acc3[hf][i][1], av[i].y, -b.y);
 #pragma unroll
                     for (int i = 0; i < MT; ++i) dmma884(acc3[hf][i][2], acc3[hf][i][3], av[i].y, b.x);
+#endif
                 }
             }
         }
@@ -317,8 +317,7 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                 for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][2], acc[hf][i][3], av[i].x + av[i].y, bs);
 #pragma unroll
                 for (int i = 0; i < MT; ++i) dmma884(q2[hf][i][0], q2[hf][i][1], av[i].y, b.y);
-                continue;
-#endif
+#else
 #pragma unroll
                 for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][0], acc[hf][i][1], av[i].x, b.x);
 #pragma unroll
@@ -327,6 +326,7 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                 for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][0], acc[hf][i][1], av[i].y, -b.y);
 #pragma unroll
                 for (int i = 0; i < MT; ++i) dmma884(acc[hf][i][2], acc[hf][i][3], av[i].y, b.x);
+#endif
             }
         }
         if (more) {

@@ -5,6 +5,7 @@ committed summaries under profiles/:
   profiles/<R>_gpu_tests.txt                            pytest -m gpu summary
   profiles/<R>_launches.csv                             ncu launch list of the bench's timed region
   profiles/<R>_leaf_ncu_details.txt                     ncu --set full of the spectral leaf kernels
+  profiles/<R>_merge_ncu_details.txt                    ncu --set full of the first 24 merge launches of a step
   profiles/traffic.json                                 dram bytes per launch (bench.py roofline.traffic)
 
     python tools/process_profiles.py r01
@@ -94,6 +95,51 @@ def leaf_ncu(r):
     json.dump(t, open(os.path.join(OUT, "traffic.json"), "w"), indent=1)
 
 
+def merge_ncu(r):
+    """profiles/<R>_merge_ncu_details.txt: one line per captured merge launch."""
+    path = os.path.join(RAW, f"{r}_merge_raw.csv")
+    if not os.path.exists(path):
+        return
+    rows = list(csv.reader(open(path).read().splitlines()))
+    h, units = rows[0], rows[1]
+    idx = {k: i for i, k in enumerate(h)}
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tmult = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+    stall = [k for k in h if k.startswith("smsp__average_warps_issue_stalled_") and
+             k.endswith("_per_issue_active.ratio")]
+    dmma = [k for k in h if "dmma" in k and k.endswith("pct_of_peak_sustained_active")]
+
+    def val(row, k, default=0.0):
+        try:
+            return float(row[idx[k]])
+        except (KeyError, ValueError):
+            return default
+
+    lines = ["# ncu --set full --clock-control none -k regex:'k_cgemm|k_gemv_sym' --launch-count 24",
+             "#   python tools/profile_step.py   (one warm c1 step: the first 24 merge launches of the step,",
+             "#   2 pole lanes of 141 half poles; cold, serialised per-launch numbers)",
+             "# columns: us | DRAM read+write MB, TB/s | warps active % | regs | FP64-pipe % | "
+             + ("DMMA-pipe % | " if dmma else "") + "L1 global ld/st sectors per request | top stalls", ""]
+    for row in rows[2:]:
+        name = row[idx["Kernel Name"]].split("(")[0].replace("void ", "").replace("rexp::dev::", "")
+        us = val(row, "gpu__time_duration.sum") * tmult.get(units[idx["gpu__time_duration.sum"]], 1.0)
+        mb = (val(row, "dram__bytes_read.sum") * mult.get(units[idx["dram__bytes_read.sum"]], 1) +
+              val(row, "dram__bytes_write.sum") * mult.get(units[idx["dram__bytes_write.sum"]], 1)) / 1e6
+        st = sorted(((val(row, k), k.replace("smsp__average_warps_issue_stalled_", "")
+                      .replace("_per_issue_active.ratio", "")) for k in stall), reverse=True)[:3]
+        dm = f"dmma {max(val(row, k) for k in dmma):4.1f}% " if dmma else ""
+        lines.append(
+            f"{name:46s} {row[idx['Grid Size']]:>13s} {us:7.1f} us {mb:7.1f} MB {mb / us if us else 0.0:4.2f} TB/s "
+            f"warps {val(row, 'sm__warps_active.avg.pct_of_peak_sustained_active'):3.0f}% "
+            f"regs {val(row, 'launch__registers_per_thread'):3.0f} "
+            f"fp64 {val(row, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active'):4.1f}% {dm}"
+            f"ld {val(row, 'l1tex__average_t_sectors_per_request_pipe_lsu_mem_global_op_ld.ratio'):4.1f} "
+            f"st {val(row, 'l1tex__average_t_sectors_per_request_pipe_lsu_mem_global_op_st.ratio'):4.1f} | "
+            + ", ".join(f"{n} {v:.1f}" for v, n in st))
+    with open(os.path.join(OUT, f"{r}_merge_ncu_details.txt"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
 def main():
     r = sys.argv[1] if len(sys.argv) > 1 else "r01"
     for src, dst in (("c1", "c1"), ("c3", "c3"), ("c2r", "c2r_wave"), ("reference", "reference")):
@@ -105,6 +151,7 @@ def main():
         open(os.path.join(OUT, f"{r}_gpu_tests.txt"), "w").write(open(t).read())
     launches(r)
     leaf_ncu(r)
+    merge_ncu(r)
 
 
 if __name__ == "__main__":

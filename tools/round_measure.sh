@@ -19,5 +19,10 @@ if python tools/profile_step.py > $O/${R}_ps.log 2>&1; then
   ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_leaf_spec \
       -o $O/${R}_leaf_full -f python tools/profile_step.py > $O/${R}_ncu_full.log 2>&1
 fi
+if [ -s $O/${R}_ps.log ]; then
+  ncu --profile-from-start off --set full --clock-control none -k regex:'k_cgemm|k_gemv_sym' --launch-count 24 \
+      -o $O/${R}_merge_full -f python tools/profile_step.py > $O/${R}_ncu_merge.log 2>&1 &&
+  ncu -i $O/${R}_merge_full.ncu-rep --page raw --csv > $O/${R}_merge_raw.csv && rm -f $O/${R}_merge_full.ncu-rep
+fi
 cat $O/${R}_gpu_tests.txt
 for f in c1 c3 c2r reference; do tail -1 $O/${R}_bench_$f.log | cut -c1-300; done
