@@ -115,6 +115,14 @@ def merge_ncu(r):
         except (KeyError, ValueError):
             return default
 
+    def count(row, k):
+        u = units[idx[k]] if k in idx else ""
+        return val(row, k) * (1e3 if u.startswith("K") else 1e6 if u.startswith("M") else 1.0)
+
+    def spr(row, op):   # L1 sectors per global request
+        req = count(row, f"l1tex__t_requests_pipe_lsu_mem_global_op_{op}.sum")
+        return count(row, f"l1tex__t_sectors_pipe_lsu_mem_global_op_{op}.sum") / req if req else 0.0
+
     lines = ["# ncu --set full --clock-control none -k regex:'k_cgemm|k_gemv_sym' --launch-count 24",
              "#   python tools/profile_step.py   (one warm c1 step: the first 24 merge launches of the step,",
              "#   2 pole lanes of 141 half poles; cold, serialised per-launch numbers)",
@@ -133,8 +141,7 @@ def merge_ncu(r):
             f"warps {val(row, 'sm__warps_active.avg.pct_of_peak_sustained_active'):3.0f}% "
             f"regs {val(row, 'launch__registers_per_thread'):3.0f} "
             f"fp64 {val(row, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active'):4.1f}% {dm}"
-            f"ld {val(row, 'l1tex__average_t_sectors_per_request_pipe_lsu_mem_global_op_ld.ratio'):4.1f} "
-            f"st {val(row, 'l1tex__average_t_sectors_per_request_pipe_lsu_mem_global_op_st.ratio'):4.1f} | "
+            f"ld {spr(row, 'ld'):4.1f} st {spr(row, 'st'):4.1f} | "
             + ", ".join(f"{n} {v:.1f}" for v, n in st))
     with open(os.path.join(OUT, f"{r}_merge_ncu_details.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
