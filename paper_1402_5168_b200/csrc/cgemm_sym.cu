@@ -59,12 +59,14 @@ void cgs_run_mode(int R2, int MT, int WN, int nst, int K, dim3 grid, cudaStream_
     (void)K;
     if (R2 == 2) cgs_tiles<16, 2, MODE>(MT, WN, nst, grid, s, a);
     else if (R2 == 4) cgs_tiles<16, 4, MODE>(MT, WN, nst, grid, s, a);
+    else if (R2 == 128) cgs_tiles<16, 128, MODE>(MT, WN, nst, grid, s, a);   // 64 RHS (c3): shifts, not divisions
     else cgs_tiles<16, 0, MODE>(MT, WN, nst, grid, s, a);
 }
 template <int MODE>
 void cgs_allow_mode() {
     cgs_allow_tiles<16, 2, MODE>();
     cgs_allow_tiles<16, 4, MODE>();
+    cgs_allow_tiles<16, 128, MODE>();
     cgs_allow_tiles<16, 0, MODE>();
 }
 
