@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
     // additive epilogue terms (LEAF_DOWN: w, DOWN: w3, UPY: child h[ext]) fetched
     // before the K loop so their latency overlaps the products
     // UP-Y with compile-time R2 uses the staged, coalesced epilogue below instead
-    constexpr bool kStagedUPY = (MODE == CG_UPY && R2T != 0);
+    constexpr bool kStagedUPY = (MODE == CG_UPY && R2T != 0 && (BN % (R2T ? R2T : 1) == 0 || (R2T ? R2T : 1) % BN == 0));
     constexpr bool kAdd = (MODE == CG_LEAF_DOWN || MODE == CG_DOWN || (MODE == CG_UPY && !kStagedUPY));
     double2 addv[kAdd ? MT : 1][kAdd ? NTW : 1][2];
     if (kAdd) {
@@ -292,15 +292,18 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
     }
 
     // UP-Y staged epilogue: the tile's additive child term h[ext] -> shared memory by
-    // cp.async now (it lands with the first operand chunk), [node][row][R2] order
+    // cp.async now (it lands with the first operand chunk), [run][row][RUN] order: a run
+    // is one node's R2 columns (R2 <= BN) or the tile's BN columns of one node (R2 > BN)
     double2* Adds = sm + cgemm_smem_bytes<MT, WN, BK, NTW, WM, NST>() / sizeof(double2);
+    constexpr int RUN = R2T == 0 ? 1 : R2T < BN ? R2T : BN;
     if constexpr (kStagedUPY) {
         constexpr int R = R2T ? R2T : 1;
-        for (int e = tid; e < (BN / R) * BM * R; e += NT) {
-            const int r2 = e % R, rl = (e / R) % BM, nl = e / (R * BM);
-            const int row = row0 + rl, col = col0 + nl * R + r2;
+        for (int e = tid; e < (BN / RUN) * BM * RUN; e += NT) {
+            const int j = e % RUN, rl = (e / RUN) % BM, nl = e / (RUN * BM);
+            const int row = row0 + rl, col = col0 + nl * RUN + j;
             if (row < a.rows && col < ncols)
-                cp_async16(Adds + e, a.add + ((size_t)m * a.add_ps + cg_child_base(a, col / R) + a.ai0[row]) * R + r2);
+                cp_async16(Adds + e,
+                           a.add + ((size_t)m * a.add_ps + cg_child_base(a, col / R) + a.ai0[row]) * R + col % R);
         }
         cp_async_commit();
     }
@@ -433,15 +436,15 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
                     Cs[((warp * NTW + n) * 8 + 2 * t4 + j) * LDC + mrow0 + i * 8 + g] =
                         make_double2(acc[i][n][j], acc[i][n][2 + j]);
         __syncthreads();
-        constexpr int NPT = BN / R2T;                  // nodes per tile
+        constexpr int NPT = BN / RUN;                  // runs per tile
         double2* dst = a.dst + (size_t)m * a.dst_ps * R2T;
-        for (int e = tid; e < NPT * BM * R2T; e += NT) {
-            const int r2 = e % R2T, rl = (e / R2T) % BM, nl = e / (R2T * BM);
-            const int row = row0 + rl, col = col0 + nl * R2T + r2;
+        for (int e = tid; e < NPT * BM * RUN; e += NT) {
+            const int j = e % RUN, rl = (e / RUN) % BM, nl = e / (RUN * BM);
+            const int row = row0 + rl, col = col0 + nl * RUN + j;
             if (row >= a.rows || col >= ncols) continue;
-            const int node = col / R2T;
+            const int node = col / R2T, r2 = col % R2T;
             const double2 ad = Adds[e];
-            const double2 v = Cs[(nl * R2T + r2) * LDC + rl];
+            const double2 v = Cs[(nl * RUN + j) * LDC + rl];
             dst[((size_t)node * a.rows + row) * R2T + r2] = make_double2(v.x + ad.x, v.y + ad.y);
         }
         return;

@@ -81,9 +81,12 @@ void cg_allow_tiles() {
 }
 
 // BK = 28 when K is a multiple of 28 (q = 14: every K of the tree), else 16;
-// R2 = 2, 4 compiled in, anything else at run time
+// R2 = 2, 4 (and 128 for up-Y / down) compiled in, anything else at run time
 // MINB bit 16: use BK = 16 even when K is a multiple of 28 (smaller shared-memory
 // footprint, more resident CTAs; an autotuner candidate)
+// R2 = 128 (64 RHS, config 3) compiled in for the first-level up-Y / down GEMMs
+// (staged up-Y epilogue, shifts instead of divisions); the levels above run the pair GEMM
+constexpr bool kR2x128 = CG_MODE == CG_UPY || CG_MODE == CG_DOWN;
 void run(int R2, int MT, int WN, int MINB, int K, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     constexpr int M = CG_MODE;
     const bool b28 = (K % 28) == 0 && !(MINB & 16);
@@ -94,6 +97,11 @@ void run(int R2, int MT, int WN, int MINB, int K, dim3 grid, cudaStream_t s, con
     } else if (R2 == 4) {
         if (b28) cg_tiles<28, 4, M>(MT, WN, MINB, grid, s, a);
         else cg_tiles<16, 4, M>(MT, WN, MINB, grid, s, a);
+    } else if (kR2x128 && R2 == 128) {
+        if constexpr (kR2x128) {
+            if (b28) cg_tiles<28, 128, M>(MT, WN, MINB, grid, s, a);
+            else cg_tiles<16, 128, M>(MT, WN, MINB, grid, s, a);
+        }
     } else {
         if (b28) cg_tiles<28, 0, M>(MT, WN, MINB, grid, s, a);
         else cg_tiles<16, 0, M>(MT, WN, MINB, grid, s, a);
@@ -104,6 +112,7 @@ void allow() {
     cg_allow_tiles<16, 2, M>(); cg_allow_tiles<28, 2, M>();
     cg_allow_tiles<16, 4, M>(); cg_allow_tiles<28, 4, M>();
     cg_allow_tiles<16, 0, M>(); cg_allow_tiles<28, 0, M>();
+    if constexpr (kR2x128) { cg_allow_tiles<16, 128, M>(); cg_allow_tiles<28, 128, M>(); }
 }
 
 }  // namespace
