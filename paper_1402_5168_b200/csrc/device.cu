@@ -851,22 +851,32 @@ struct RecoverArgs {
     double c1, s0, s1;      // RSW: P, Q ; WAVE: B1
 };
 
-__device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, long long g, double& gx, double& gy) {
+// gradient of NR consecutive planes (stride N) of one field at node g: the
+// element-map indices and derivative weights are loaded once for all NR planes
+template <int NR>
+__device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, long long g, double* gx, double* gy) {
     const int p = a.p, q = a.q, n = a.n;
     const int q2 = q * q;
+    const long long N = a.N;
+    auto fma_r = [&](double* acc, double w, long long idx) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[r] += w * Ef[r * N + idx];
+    };
+    double s0[NR], s1[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) s0[r] = s1[r] = 0.0;
     if (g < a.NI) {
         const int e = (int)(g / q2);
         const int rr = (int)(g % q2);
         const int i = rr % q + 1, j = rr / q + 1;
         const int* eg = a.elem_g + (size_t)e * p * p;
-        double sx = 0.0, sy = 0.0;
-#pragma unroll 8
+#pragma unroll 4
         for (int k = 0; k < p; ++k) {
-            sx += a.D[i * p + k] * Ef[eg[j * p + k]];
-            sy += a.D[j * p + k] * Ef[eg[k * p + i]];
+            fma_r(s0, a.D[i * p + k], eg[j * p + k]);
+            fma_r(s1, a.D[j * p + k], eg[k * p + i]);
         }
-        gx = a.c1 * sx;
-        gy = a.c1 * sy;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) { gx[r] = a.c1 * s0[r]; gy[r] = a.c1 * s1[r]; }
         return;
     }
     const bool vert = g < a.NI + a.NV;
@@ -879,67 +889,81 @@ __device__ __forceinline__ void grad_at(const RecoverArgs& a, const double* Ef, 
         const int eL = ey * n + (ex + n - 1) % n;
         const int* eg = E_of(e);
         const int* egL = E_of(eL);
-        double sr = 0.0, sl = 0.0;
-#pragma unroll 8
+#pragma unroll 4
         for (int k = 0; k < p; ++k) {
-            sr += a.D[0 * p + k] * Ef[eg[t * p + k]];
-            sl += a.D[(p - 1) * p + k] * Ef[egL[t * p + k]];
+            fma_r(s0, a.D[0 * p + k], eg[t * p + k]);
+            fma_r(s1, a.D[(p - 1) * p + k], egL[t * p + k]);
         }
-        gx = 0.5 * a.c1 * (sr + sl);
+        double st[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) { gx[r] = 0.5 * a.c1 * (s0[r] + s1[r]); st[r] = 0.0; }
         const int eBn = ((ey + n - 1) % n) * n + ex, eTn = ((ey + 1) % n) * n + ex;
-        double st = a.Dw[(t - 1) * p + 0] * Ef[a.NI + (long long)eBn * q + (q - 1)];
-#pragma unroll 8
-        for (int l = 1; l <= q; ++l) st += a.Dw[(t - 1) * p + l] * Ef[a.NI + (long long)e * q + (l - 1)];
-        st += a.Dw[(t - 1) * p + (p - 1)] * Ef[a.NI + (long long)eTn * q + 0];
-        gy = a.c1 * st;
+        fma_r(st, a.Dw[(t - 1) * p + 0], a.NI + (long long)eBn * q + (q - 1));
+#pragma unroll 4
+        for (int l = 1; l <= q; ++l) fma_r(st, a.Dw[(t - 1) * p + l], a.NI + (long long)e * q + (l - 1));
+        fma_r(st, a.Dw[(t - 1) * p + (p - 1)], a.NI + (long long)eTn * q + 0);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) gy[r] = a.c1 * st[r];
     } else {
         const int eB = ((ey + n - 1) % n) * n + ex;
         const int* eg = E_of(e);
         const int* egB = E_of(eB);
-        double st_ = 0.0, sb = 0.0;
-#pragma unroll 8
+#pragma unroll 4
         for (int k = 0; k < p; ++k) {
-            st_ += a.D[0 * p + k] * Ef[eg[k * p + t]];
-            sb += a.D[(p - 1) * p + k] * Ef[egB[k * p + t]];
+            fma_r(s0, a.D[0 * p + k], eg[k * p + t]);
+            fma_r(s1, a.D[(p - 1) * p + k], egB[k * p + t]);
         }
-        gy = 0.5 * a.c1 * (st_ + sb);
+        double sx[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) { gy[r] = 0.5 * a.c1 * (s0[r] + s1[r]); sx[r] = 0.0; }
         const int eLn = ey * n + (ex + n - 1) % n, eRn = ey * n + (ex + 1) % n;
         const long long hb = a.NI + a.NV;
-        double sx = a.Dw[(t - 1) * p + 0] * Ef[hb + (long long)eLn * q + (q - 1)];
-#pragma unroll 8
-        for (int l = 1; l <= q; ++l) sx += a.Dw[(t - 1) * p + l] * Ef[hb + (long long)e * q + (l - 1)];
-        sx += a.Dw[(t - 1) * p + (p - 1)] * Ef[hb + (long long)eRn * q + 0];
-        gx = a.c1 * sx;
+        fma_r(sx, a.Dw[(t - 1) * p + 0], hb + (long long)eLn * q + (q - 1));
+#pragma unroll 4
+        for (int l = 1; l <= q; ++l) fma_r(sx, a.Dw[(t - 1) * p + l], hb + (long long)e * q + (l - 1));
+        fma_r(sx, a.Dw[(t - 1) * p + (p - 1)], hb + (long long)eRn * q + 0);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) gx[r] = a.c1 * sx[r];
     }
 }
 
+// one thread per (node, NR consecutive planes r2 = 2 k + part); node-fastest so a
+// warp reads neighbouring nodes of the same planes
+template <int NR>
 __global__ void k_recover(RecoverArgs a) {
-    // node-fastest threads: a warp reads neighbouring nodes of one E plane
     const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (tid >= a.N * a.R2) return;
+    if (tid >= a.N * (a.R2 / NR)) return;
     const long long g = tid % a.N;
-    const int r2 = (int)(tid / a.N);
-    const int k = r2 >> 1, part = r2 & 1;
-    double* base = a.u + (size_t)k * 3 * a.N * 2 + part;
-    const double* E0 = a.E + ((size_t)0 * a.R2 + r2) * a.N;
-    const double* E1 = a.E + ((size_t)1 * a.R2 + r2) * a.N;
-    double g1x, g1y;
-    grad_at(a, E1, g, g1x, g1y);
+    const int r0 = (int)(tid / a.N) * NR;
+    const double* E0 = a.E + ((size_t)0 * a.R2 + r0) * a.N;
+    const double* E1 = a.E + ((size_t)1 * a.R2 + r0) * a.N;
+    double g1x[NR], g1y[NR];
+    grad_at<NR>(a, E1, g, g1x, g1y);
     if (a.model == 0) {
-        const double* E2 = a.E + ((size_t)2 * a.R2 + r2) * a.N;
-        double g2x, g2y;
-        grad_at(a, E2, g, g2x, g2y);
-        const double v1 = base[(size_t)g * 2], v2 = base[((size_t)a.N + g) * 2];
+        const double* E2 = a.E + ((size_t)2 * a.R2 + r0) * a.N;
+        double g2x[NR], g2y[NR];
+        grad_at<NR>(a, E2, g, g2x, g2y);
         const double P = a.s0, Q = a.s1;
-        base[(size_t)g * 2] = g1x + g2y - P * v1 - Q * v2;
-        base[((size_t)a.N + g) * 2] = g1y - g2x - P * v2 + Q * v1;
-        base[((size_t)2 * a.N + g) * 2] = E0[g];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int r2 = r0 + r, k = r2 >> 1, part = r2 & 1;
+            double* base = a.u + (size_t)k * 3 * a.N * 2 + part;
+            const double v1 = base[(size_t)g * 2], v2 = base[((size_t)a.N + g) * 2];
+            base[(size_t)g * 2] = g1x[r] + g2y[r] - P * v1 - Q * v2;
+            base[((size_t)a.N + g) * 2] = g1y[r] - g2x[r] - P * v2 + Q * v1;
+            base[((size_t)2 * a.N + g) * 2] = E0[(size_t)r * a.N + g];
+        }
     } else {
-        const double w0 = base[(size_t)g * 2], z0 = base[((size_t)a.N + g) * 2];
         const double B1 = a.s0;
-        base[(size_t)g * 2] = g1x - B1 * w0;
-        base[((size_t)a.N + g) * 2] = g1y - B1 * z0;
-        base[((size_t)2 * a.N + g) * 2] = E0[g];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int r2 = r0 + r, k = r2 >> 1, part = r2 & 1;
+            double* base = a.u + (size_t)k * 3 * a.N * 2 + part;
+            const double w0 = base[(size_t)g * 2], z0 = base[((size_t)a.N + g) * 2];
+            base[(size_t)g * 2] = g1x[r] - B1 * w0;
+            base[((size_t)a.N + g) * 2] = g1y[r] - B1 * z0;
+            base[((size_t)2 * a.N + g) * 2] = E0[(size_t)r * a.N + g];
+        }
     }
 }
 
@@ -2125,9 +2149,12 @@ int DeviceStore::recover(const double* d_E_in, double* d_state, cudaStream_t s) 
     a.model = model; a.n = n; a.p = p; a.q = q; a.R2 = R2; a.N = N; a.NI = NI; a.NV = NV; a.c1 = c1;
     a.s0 = scal.size() > 0 ? scal[0] : 0.0;
     a.s1 = scal.size() > 1 ? scal[1] : 0.0;
-    const long long tot = N * R2;
+    // planes per thread: 2 (a complex value's re / im) or 8 (many right-hand sides)
+    const int nr = R2 % 8 == 0 ? 8 : 2;
+    const long long tot = N * (R2 / nr);
     tbeg(s);
-    k_recover<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
+    if (nr == 8) k_recover<8><<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
+    else k_recover<2><<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(a);
     tend(T_RECOVER, s);
     return check("recover");
 }
