@@ -32,9 +32,11 @@ Readings of the paper taken here (all listed in DESIGN.md §3):
       L_2 repeats L_1, PAPER.md:520 - a typo).
   R4  Scaled variable x = y / (2 pi): e^{iy} = e^{2 pi i x}, A = tau*Lambda
       maps to X = A / (2 pi) (§3.1 works with e^{2 pi i x}).
-  R5  Parameter policy (paper gives no h):  h = 0.17, hS = 2h,
-      M0 = ceil(X / hS) + 10, M = ceil(M0 hS / h).  The filter lattice hS
-      differs from h so the poles of S and R are distinct (§3.3).
+  R5  Parameter policy (paper gives no h):  h = 0.17, hS = 2.5 h,
+      M0 = ceil(X / hS) + c, M = ceil(M0 hS / h), with c the smallest margin
+      >= 8 for which the approximant passes the delta / 1 + delta checks of
+      §1.2 (Eqs. "RM_prop1", "RM_prop2").  The filter lattice hS differs from
+      h so the poles of S and R are distinct (§3.3).
   R6  Stability filter = §3.3's first construction, the product S(iy)R(iy)
       written as one proper rational function (union of pole sets, residue of
       each factor multiplied by the other factor evaluated at the pole).
@@ -238,40 +240,53 @@ def product_rational(pS, rS, pR, rR):
 # build: the (alpha_m, b_m) of exp(tau L) ~ sum_m b_m (tau L - alpha_m)^{-1}
 # ---------------------------------------------------------------------------
 H_DEFAULT = 0.17
-M0_MARGIN = 10
+HS_RATIO = 2.5
+M0_MARGIN_MIN = 8
+M0_MARGIN_MAX = 16
 
 
-def exp_approx_params(A):
+def exp_approx_params(A, margin=M0_MARGIN_MIN):
     """Reading R5: parameter policy for the interval [-A, A] (A = tau*Lambda)."""
     X = A / (2.0 * math.pi)
     h = H_DEFAULT
-    hS = 2.0 * h
-    M0 = int(math.ceil(X / hS)) + M0_MARGIN
+    hS = HS_RATIO * h
+    M0 = int(math.ceil(X / hS)) + margin
     M = int(math.ceil(M0 * hS / h - 1e-9))
-    return dict(X=X, h=h, hS=hS, M=M, M0=M0)
+    return dict(X=X, h=h, hS=hS, M=M, M0=M0, margin=margin)
+
+
+def _check(poles, res, A, nsamp_per_unit):
+    """Sup error against e^{iy} on |y| <= A and sup |R(iy)| on the real line
+    (dense sampling, the paper's own verification style, Figs. 3-5)."""
+    y = np.linspace(-A, A, int(2 * A * nsamp_per_unit) + 1)
+    err = np.abs(rational_eval(poles, res, 1j * y) - np.exp(1j * y)).max()
+    far = np.concatenate([np.linspace(-4 * A - 60, 4 * A + 60, int(8 * A * nsamp_per_unit) + 1),
+                          np.logspace(0, 7, 400), -np.logspace(0, 7, 400)])
+    maxmod = max(np.abs(rational_eval(poles, res, 1j * far)).max(),
+                 np.abs(rational_eval(poles, res, 1j * y)).max())
+    return float(err), float(maxmod)
 
 
 def build_exp_approx(A, delta, verify=True, nsamp_per_unit=32):
     """Poles alpha_m and weights b_m with |e^{iy} - R(iy)| <= delta on |y| <= A
     and |R(iy)| <= 1 + delta on the real line (§1.2 Eqs. "RM_prop1", "RM_prop2").
 
-    R = S * R_gauss  (reading R6).  Verification by dense sampling, the
-    paper's own verification style (Figs. 3-5).
+    R = S * R_gauss  (reading R6); the filter margin c of reading R5 grows
+    from 8 until both checks pass (they always run: they pick c).  With
+    verify=True a failure at the largest margin raises.
     Returns dict(poles, res, params, err, maxmod).
     """
-    prm = exp_approx_params(A)
-    h, hS, M, M0 = prm["h"], prm["hS"], prm["M"], prm["M0"]
-    pR, rR = compose_rational(h, gaussian_coeffs_exp(h, M))
-    pS, rS = compose_rational(hS, gaussian_coeffs_chi(M0))
-    poles, res = product_rational(pS, rS, pR, rR)
-    out = dict(poles=poles, res=res, params=prm, err=None, maxmod=None)
+    for margin in range(M0_MARGIN_MIN, M0_MARGIN_MAX + 1):
+        prm = exp_approx_params(A, margin)
+        h, hS, M, M0 = prm["h"], prm["hS"], prm["M"], prm["M0"]
+        pR, rR = compose_rational(h, gaussian_coeffs_exp(h, M))
+        pS, rS = compose_rational(hS, gaussian_coeffs_chi(M0))
+        poles, res = product_rational(pS, rS, pR, rR)
+        err, maxmod = _check(poles, res, A, nsamp_per_unit)
+        if err <= delta and maxmod <= 1.0 + delta:
+            break
+    out = dict(poles=poles, res=res, params=prm, err=err, maxmod=maxmod)
     if verify:
-        y = np.linspace(-A, A, int(2 * A * nsamp_per_unit) + 1)
-        err = np.abs(rational_eval(poles, res, 1j * y) - np.exp(1j * y)).max()
-        far = np.concatenate([np.linspace(-4 * A - 60, 4 * A + 60, int(8 * A * nsamp_per_unit) + 1),
-                              np.logspace(0, 7, 400), -np.logspace(0, 7, 400)])
-        maxmod = np.abs(rational_eval(poles, res, 1j * far)).max()
-        out["err"], out["maxmod"] = float(err), float(maxmod)
         if err > delta:
             raise ValueError(f"rational approximation error {err:.3e} exceeds delta={delta:.1e}")
         if maxmod > 1.0 + delta:

@@ -163,14 +163,29 @@ def apply(handle: Handle, u, nsteps, stream=None):
     return u
 
 
+def _check_sharded_args(handle: Handle, u, e):
+    import torch
+    dev = u.device if isinstance(u, torch.Tensor) else None
+    if not (isinstance(u, torch.Tensor) and u.is_cuda and u.dtype == torch.complex128 and u.is_contiguous()
+            and u.numel() == handle.nrhs * 3 * handle.N):
+        raise ValueError("u must be a contiguous CUDA complex128 tensor of size nrhs*3*N")
+    if not (isinstance(e, torch.Tensor) and e.is_cuda and e.dtype == torch.float64 and e.is_contiguous()
+            and e.numel() == handle.partial_len):
+        raise ValueError("e must be a contiguous CUDA float64 tensor of length partial_len")
+    if e.device != dev or (handle.device >= 0 and dev.index != handle.device):
+        raise ValueError("u and e must live on the handle's device")
+
+
 def step_partial(handle: Handle, u, e, stream=None):
     """Pole-sharded step, part 1: this handle's pole sums into e (CUDA float64, partial_len)."""
+    _check_sharded_args(handle, u, e)
     _lib.check(_lib.load().rexp_step_partial(handle.ptr, u.data_ptr(), e.data_ptr(),
                                              ctypes.c_void_p(_stream_ptr(stream))), "rexp_step_partial")
 
 
 def step_finish(handle: Handle, e, u, stream=None):
     """Pole-sharded step, part 2: recover the new state from the all-reduced pole sums."""
+    _check_sharded_args(handle, u, e)
     _lib.check(_lib.load().rexp_step_finish(handle.ptr, e.data_ptr(), u.data_ptr(),
                                             ctypes.c_void_p(_stream_ptr(stream))), "rexp_step_finish")
 

@@ -30,6 +30,7 @@ def build(force=False, verbose_ptxas=False):
     os.makedirs(BUILD, exist_ok=True)
     srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     srcs.append(os.path.join(os.path.dirname(HERE), "include", "rexp.h"))
+    srcs.append(os.path.abspath(__file__))     # compile flags live here
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(s) <= t for s in srcs):

@@ -13,14 +13,10 @@
 
 namespace rexp {
 namespace {
-std::mutex g_err_mu;
-std::string g_err;
-thread_local std::string t_err_copy;
+// one message per calling thread (include/rexp.h: "thread-local")
+thread_local std::string t_err;
 }  // namespace
-void set_error(const std::string& msg) {
-    std::lock_guard<std::mutex> lk(g_err_mu);
-    g_err = msg;
-}
+void set_error(const std::string& msg) { t_err = msg; }
 }  // namespace rexp
 
 struct rexp_handle {
@@ -40,11 +36,7 @@ using namespace rexp;
 
 extern "C" {
 
-const char* rexp_last_error(void) {
-    std::lock_guard<std::mutex> lk(g_err_mu);
-    t_err_copy = g_err;
-    return t_err_copy.c_str();
-}
+const char* rexp_last_error(void) { return t_err.c_str(); }
 
 void rexp_default_options(rexp_options* opt) {
     if (!opt) return;
@@ -223,12 +215,20 @@ int64_t rexp_partial_len(const rexp_handle* h) {
 int rexp_step_partial(rexp_handle* h, const double* u_dev, double* e_dev, void* stream) {
     int rc = need_device(h, false);
     if (rc) return rc;
+    if (!u_dev || !e_dev) {
+        set_error("rexp_step_partial: null state or pole-sum pointer");
+        return REXP_EINVAL;
+    }
     return h->dev->solve_sum(u_dev, e_dev, static_cast<cudaStream_t>(stream));
 }
 
 int rexp_step_finish(rexp_handle* h, const double* e_dev, double* u_dev, void* stream) {
     int rc = need_device(h, false);
     if (rc) return rc;
+    if (!u_dev || !e_dev) {
+        set_error("rexp_step_finish: null state or pole-sum pointer");
+        return REXP_EINVAL;
+    }
     return h->dev->recover(e_dev, u_dev, static_cast<cudaStream_t>(stream));
 }
 

@@ -98,61 +98,67 @@ int build_exp_approx(double A, double delta, RationalApprox& out) {
         set_error("build_exp_approx: need tau*Lambda > 0 and delta > 0");
         return REXP_EINVAL;
     }
-    // Reading R5: h = 0.17, hS = 2h, M0 = ceil(X/hS) + 10, M = ceil(M0 hS / h), X = A/(2 pi).
+    // Reading R5: h = 0.17, hS = 2.5 h, M0 = ceil(X/hS) + c, M = ceil(M0 hS / h),
+    // X = A/(2 pi); the margin c grows from 8 until both checks below pass.
     const double X = A / (2.0 * kPi);
-    const double h = 0.17, hS = 2.0 * h;
-    const int M0 = static_cast<int>(std::ceil(X / hS)) + 10;
-    const int M = static_cast<int>(std::ceil(M0 * hS / h - 1e-9));
-    // R_gauss: c_m = (h/psihat_h(1)) e^{-2 pi i m h}
-    std::vector<cd> c(2 * M + 1);
-    for (int m = -M; m <= M; ++m)
-        c[m + M] = (h / psihat(1.0, h)) * std::exp(cd(0.0, -2.0 * kPi * m * h));
-    // S ~ chi: unit coefficients (Eq. "partition of unity-1")
-    std::vector<cd> cS(2 * M0 + 1, cd(1.0, 0.0));
-    std::vector<cd> pR, rR, pS, rS;
-    compose(h, c, pR, rR);
-    compose(hS, cS, pS, rS);
-    // product S*R as a proper rational function (reading R6)
-    double gap = 1e300;
-    for (auto& a : pS)
-        for (auto& b : pR) gap = std::min(gap, std::abs(a - b));
-    if (gap < 1e-8) {
-        set_error("build_exp_approx: pole collision between filter and approximant");
-        return REXP_EACCURACY;
-    }
-    out.poles.clear();
-    out.res.clear();
-    for (size_t k = 0; k < pS.size(); ++k) {
-        out.poles.push_back(pS[k]);
-        out.res.push_back(rS[k] * rational_eval(pR, rR, pS[k]));
-    }
-    for (size_t k = 0; k < pR.size(); ++k) {
-        out.poles.push_back(pR[k]);
-        out.res.push_back(rR[k] * rational_eval(pS, rS, pR[k]));
-    }
-    out.h = h;
-    out.hS = hS;
-    out.M = M;
-    out.M0 = M0;
-    // verification by dense sampling (paper's own style, Figs. 3-5)
+    const double h = 0.17, hS = 2.5 * h;
     double err = 0.0, mx = 0.0;
-    const int nin = static_cast<int>(2 * A * 32) + 1;
-    for (int k = 0; k < nin; ++k) {
-        const double y = -A + 2.0 * A * k / (nin - 1);
-        const cd v = rational_eval(out.poles, out.res, cd(0.0, y));
-        err = std::max(err, std::abs(v - std::exp(cd(0.0, y))));
-        mx = std::max(mx, std::abs(v));
-    }
-    const double Y = 4 * A + 60;
-    const int nfar = static_cast<int>(8 * A * 32) + 1;
-    for (int k = 0; k < nfar; ++k) {
-        const double y = -Y + 2.0 * Y * k / (nfar - 1);
-        mx = std::max(mx, std::abs(rational_eval(out.poles, out.res, cd(0.0, y))));
-    }
-    for (int k = 0; k < 400; ++k) {
-        const double y = std::pow(10.0, 7.0 * k / 399.0);
-        mx = std::max(mx, std::abs(rational_eval(out.poles, out.res, cd(0.0, y))));
-        mx = std::max(mx, std::abs(rational_eval(out.poles, out.res, cd(0.0, -y))));
+    for (int margin = 8; margin <= 16; ++margin) {
+        const int M0 = static_cast<int>(std::ceil(X / hS)) + margin;
+        const int M = static_cast<int>(std::ceil(M0 * hS / h - 1e-9));
+        // R_gauss: c_m = (h/psihat_h(1)) e^{-2 pi i m h}
+        std::vector<cd> c(2 * M + 1);
+        for (int m = -M; m <= M; ++m)
+            c[m + M] = (h / psihat(1.0, h)) * std::exp(cd(0.0, -2.0 * kPi * m * h));
+        // S ~ chi: unit coefficients (Eq. "partition of unity-1")
+        std::vector<cd> cS(2 * M0 + 1, cd(1.0, 0.0));
+        std::vector<cd> pR, rR, pS, rS;
+        compose(h, c, pR, rR);
+        compose(hS, cS, pS, rS);
+        // product S*R as a proper rational function (reading R6)
+        double gap = 1e300;
+        for (auto& a : pS)
+            for (auto& b : pR) gap = std::min(gap, std::abs(a - b));
+        if (gap < 1e-8) {
+            set_error("build_exp_approx: pole collision between filter and approximant");
+            return REXP_EACCURACY;
+        }
+        out.poles.clear();
+        out.res.clear();
+        for (size_t k = 0; k < pS.size(); ++k) {
+            out.poles.push_back(pS[k]);
+            out.res.push_back(rS[k] * rational_eval(pR, rR, pS[k]));
+        }
+        for (size_t k = 0; k < pR.size(); ++k) {
+            out.poles.push_back(pR[k]);
+            out.res.push_back(rR[k] * rational_eval(pS, rS, pR[k]));
+        }
+        out.h = h;
+        out.hS = hS;
+        out.M = M;
+        out.M0 = M0;
+        // verification by dense sampling (paper's own style, Figs. 3-5)
+        err = 0.0;
+        mx = 0.0;
+        const int nin = static_cast<int>(2 * A * 32) + 1;
+        for (int k = 0; k < nin; ++k) {
+            const double y = -A + 2.0 * A * k / (nin - 1);
+            const cd v = rational_eval(out.poles, out.res, cd(0.0, y));
+            err = std::max(err, std::abs(v - std::exp(cd(0.0, y))));
+            mx = std::max(mx, std::abs(v));
+        }
+        const double Y = 4 * A + 60;
+        const int nfar = static_cast<int>(8 * A * 32) + 1;
+        for (int k = 0; k < nfar; ++k) {
+            const double y = -Y + 2.0 * Y * k / (nfar - 1);
+            mx = std::max(mx, std::abs(rational_eval(out.poles, out.res, cd(0.0, y))));
+        }
+        for (int k = 0; k < 400; ++k) {
+            const double y = std::pow(10.0, 7.0 * k / 399.0);
+            mx = std::max(mx, std::abs(rational_eval(out.poles, out.res, cd(0.0, y))));
+            mx = std::max(mx, std::abs(rational_eval(out.poles, out.res, cd(0.0, -y))));
+        }
+        if (err <= delta && mx <= 1.0 + delta) break;
     }
     out.err = err;
     out.maxmod = mx;

@@ -162,7 +162,16 @@ def test_step_linearity_and_half_pole_identity(op16):
 
 
 def test_poles_counts_match_policy():
-    ap = build_exp_approx(20.0, 1e-10)
-    assert len(ap["poles"]) == 332
-    ap = build_exp_approx(60.0, 1e-10)
-    assert len(ap["poles"]) == 560
+    """Reading R5: hS = 2.5 h and the smallest filter margin >= 8 that passes the
+    delta / 1 + delta checks (a smaller margin fails them)."""
+    from oracle.rational import M0_MARGIN_MIN, _check, compose_rational, exp_approx_params, \
+        gaussian_coeffs_chi, gaussian_coeffs_exp, product_rational
+    for A, npoles, margin in [(20.0, 316, 8), (60.0, 528, 8), (100.0, 736, 8), (160.0, 1060, 9), (10.0, 276, 9)]:
+        ap = build_exp_approx(A, 1e-10)
+        assert len(ap["poles"]) == npoles and ap["params"]["margin"] == margin, A
+        if margin > M0_MARGIN_MIN:
+            prm = exp_approx_params(A, margin - 1)
+            pR, rR = compose_rational(prm["h"], gaussian_coeffs_exp(prm["h"], prm["M"]))
+            pS, rS = compose_rational(prm["hS"], gaussian_coeffs_chi(prm["M0"]))
+            err, mm = _check(*product_rational(pS, rS, pR, rR), A, 32)
+            assert err > 1e-10 or mm > 1 + 1e-10
