@@ -32,7 +32,7 @@ from workloads import CONFIGS, initial_state, wave_speed_field  # noqa: E402
 BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
 UNIT = "dof-steps/s"
-DEFAULT_CONFIG = "c1_rsw_16x16_p16"
+DEFAULT_CONFIG = "c3_rsw_32x32_p16_x64"   # the largest single-GPU BASELINE config
 
 
 def peaks():
@@ -170,73 +170,135 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
     return w
 
 
-def roofline_for(cfg, h, times, steps, pk):
-    """Dominant kernel = the class with the largest device time.  achieved =
-    algorithmic work per launch / average launch time (CUDA events on the
-    launching stream)."""
-    nh = h.num_half_poles
+# FP64 peaks of this pool's B200 (MEASURED_PEAKS.json has no FP64 entry): measured
+# with tools/fp64_peak.cu (profiles/r01_fp64_peak.txt); nominal 148 SMs x 64 FMA/clk
+# x 2 x 1965 MHz = 37.2 TFLOP/s for both pipes.
+FP64_DMMA_PEAK = 37.2
+FP64_DFMA_PEAK = 35.93
+PEAK_SOURCE = ("FP64: tools/fp64_peak.cu on this pool's B200 (profiles/r01_fp64_peak.txt): mma.sync.m8n8k4.f64 "
+               "37.2, DFMA 35.93 TFLOP/s (= nominal 148 SM x 64 FMA x 2 x 1.965 GHz); HBM: MEASURED_PEAKS.json")
+
+
+def class_bound(cls, shared, R2):
+    """Which unit bounds a kernel class: the shared store's merge
+    stages are DMMA GEMMs (k_cgemm / k_cgemm_sym; a few-RHS run's top levels are
+    HBM-bound pair GEMVs), the spectral leaf kernels and the Fourier root run on
+    the FP64 FMA pipe; the per-node store streams its operators (HBM)."""
+    if not shared:
+        return "hbm"
+    if cls in ("merge_up", "merge_down"):
+        return "tensor"
+    return "alu"
+
+
+def state_bytes(cfg, nh, R2, shared, nF=3, nE=3):
+    """Algorithmic bytes of the per-pole state each class must move per step
+    (complex128 values x R2 real right-hand sides):
+      merge up   X: read h^a_3, h^b_3 (2 n3), write w3 (n3); Y: read h_child[ext]
+                 (next) and w3 (n3), write h (next)
+      merge down read u_ext (next) and w3 (n3), write u3 (n3)
+      root       read the 2 seam blocks of h (2 * 2nq), write s (2nq)
+      leaf up    write the leaf flux (4q per leaf); read the RHS fields (nF q^2 reals) once per step
+      leaf down  read the leaf's edge values (4q per leaf); write the pole sums (nE q^2 reals) once per step
+    """
+    n, q = cfg["n"], cfg["p"] - 2
+    e = n * n
+    lv = tree_dims(n, q)
+    c = 16 * R2
+    up = sum(nh * nd * (3 * n3 + 2 * nx + n3) * c for nd, n3, nx in lv)
+    down = sum(nh * nd * (nx + 2 * n3) * c for nd, n3, nx in lv)
+    root = nh * 3 * 2 * n * q * c
+    leaf_up = nh * e * 4 * q * c + e * nF * q * q * 8 * R2
+    leaf_down = nh * e * 4 * q * c + e * nE * q * q * 8 * R2
+    return {"merge_up": up, "merge_down": down, "root": root, "leaf_up": leaf_up, "leaf_down": leaf_down}
+
+
+def roofline_for(cfg, workload, h, times, steps, pk, step_ms, nh_here=None):
+    """Dominant kernel = the class with the largest share of device time per
+    step (CUDA events around every launch, on the launching stream).  achieved
+    = algorithmic work per launch (class_work: flops, operator bytes; plus the
+    per-pole state bytes of state_bytes) / average launch duration."""
+    nh = nh_here or h.num_half_poles          # the half poles this handle applies
     R2 = 2 * h.nrhs
     shared = (cfg["model"] == "rsw")
     nF, nE = (3, 3) if cfg["model"] == "rsw" else (2, 2)
     work = class_work(cfg, nh, R2, shared, leaf=h.leaf_solver or "dense", nF=nF, nE=nE)
-    # dominant kernel = the single launch with the largest average duration
-    # (the merge tree is many launches of different shapes; it is reported per class)
-    # (among the classes with a work model: the per-step pre/recover/pole-sum
-    # kernels are small and bandwidth-trivial)
-    dom = max((k for k in times if times[k][1] and k in work), key=lambda k: times[k][0] / times[k][1])
-    ms, nl = times[dom]
-    per_launch_ms = ms / max(nl, 1)
-    # the spectral leaf kernels run on the FP64 FMA pipe: measured DFMA 35.9 TFLOP/s
-    # (profiles/r01_fp64_peak.txt; nominal 148 SMs x 64 FMA/clk x 2 x 1965 MHz = 37.2)
-    fp64_peak = 35.93
+    sbytes = state_bytes(cfg, nh, R2, shared, nF, nE)
+    hbm = pk.get("hbm_gbs", 6549.8)
+    total_ms = sum(t for t, c in times.values())
     per_class = {}
     for k, (t, c) in times.items():
-        if k in work and c:
+        if not c:
+            continue
+        d = {"share": round(t / total_ms, 4), "ms_per_step": round(t / steps, 4), "launches_per_step": c / steps}
+        if k in work:
             fl, by = work[k]
-            launches_per_step = c / steps
-            sec = t / c * 1e-3
-            per_class[k] = {"tflops": round(fl / launches_per_step / sec / 1e12, 3),
-                            "operator_GBps": round(by / launches_per_step / sec / 1e9, 1)}
-    if dom not in work:
-        return {"kernel": dom, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
-                "traffic": None, "per_class": per_class}
-    fl, by = work[dom]
+            sb = sbytes.get(k, 0)
+            sec = t / steps * 1e-3
+            bound = class_bound(k, shared, R2)
+            pkf = FP64_DMMA_PEAK if bound == "tensor" else FP64_DFMA_PEAK
+            d.update({"bound": bound, "gflop_per_step": round(fl / 1e9, 3), "tflops": round(fl / sec / 1e12, 3),
+                      "frac_fp64": round(fl / sec / 1e12 / pkf, 4),
+                      "operator_GB_per_step": round(by / 1e9, 4), "state_GB_per_step": round(sb / 1e9, 4),
+                      "GBps": round((by + sb) / sec / 1e9, 1), "frac_hbm": round((by + sb) / sec / 1e9 / hbm, 4)})
+        per_class[k] = d
+    dom = max((k for k in per_class if k in work), key=lambda k: times[k][0])
+    ms, nl = times[dom]
+    per_launch_ms = ms / max(nl, 1)
     lps = nl / steps
-    if shared:
+    fl, by = work[dom]
+    bound = class_bound(dom, shared, R2)
+    out = {"kernel": dom, "share_of_step": per_class[dom]["share"], "bound": bound,
+           "per_launch_ms": round(per_launch_ms, 4), "launches_per_step": lps, "peak_source": PEAK_SOURCE,
+           "traffic": traffic_for(workload, dom),
+           "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (profiles/traffic.json)"}
+    if bound == "hbm":
+        ach = (by + sbytes.get(dom, 0)) / lps / (per_launch_ms * 1e-3) / 1e9
+        out.update({"achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                    "algorithmic_bytes_per_launch": (by + sbytes.get(dom, 0)) / lps})
+    else:
+        pkf = FP64_DMMA_PEAK if bound == "tensor" else FP64_DFMA_PEAK
         ach = fl / lps / (per_launch_ms * 1e-3) / 1e12
-        return {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(fp64_peak, 2),
-                "unit": "TFLOP/s", "frac": round(ach / fp64_peak, 4), "traffic": traffic_for(dom),
-                "peak_source": "measured DFMA 35.93 TF (profiles/r01_fp64_peak.txt, tools/fp64_peak.cu); nominal 37.2",
-                "per_launch_ms": round(per_launch_ms, 4), "per_class": per_class}
-    hbm = pk.get("hbm_gbs", 6650.0)
-    ach = by / lps / (per_launch_ms * 1e-3) / 1e9
-    return {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(ach / hbm, 4), "traffic": traffic_for(dom), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-            "per_launch_ms": round(per_launch_ms, 4), "per_class": per_class}
+        out.update({"achieved": round(ach, 3), "peak": pkf, "unit": "TFLOP/s", "frac": round(ach / pkf, 4),
+                    "algorithmic_flops_per_launch": fl / lps})
+    # whole step: every class's algorithmic work over the timed step time
+    fl_all = sum(v[0] for v in work.values())
+    by_all = sum(v[1] for v in work.values()) + sum(sbytes.values())
+    out["whole_step"] = {"gflop": round(fl_all / 1e9, 2), "tflops": round(fl_all / (step_ms * 1e-3) / 1e12, 3),
+                         "frac_fp64_tensor": round(fl_all / (step_ms * 1e-3) / 1e12 / FP64_DMMA_PEAK, 4),
+                         "GB": round(by_all / 1e9, 3), "GBps": round(by_all / (step_ms * 1e-3) / 1e9, 1),
+                         "frac_hbm": round(by_all / (step_ms * 1e-3) / 1e9 / hbm, 4)}
+    out["per_class"] = per_class
+    return out
 
 
-def traffic_for(kernel):
-    """dram read+write bytes per launch from the committed ncu --set full capture, if any."""
+def traffic_for(workload, kernel):
+    """dram read+write bytes per launch of `kernel` in `workload`, from the committed
+    ncu --set full capture (profiles/traffic.json, keyed "workload/class"), else None."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        return d.get(kernel)
+        return d.get(f"{workload}/{kernel}")
     except Exception:
         return None
 
 
-def oracle_sample(cfg, npoles_sample, seconds_budget=30.0):
-    """Time the CPU oracle on a bounded sample: `npoles_sample` of the poles,
-    factorization untimed (it is the setup), one resolvent apply each timed;
-    the full-step time is extrapolated by the total pole count."""
+def oracle_sample(cfg, npoles_sample=None, nrhs_sample=2):
+    """Time the CPU oracle on a bounded sample: `npoles_sample` of the poles
+    (factorization untimed: it is the setup), one resolvent apply each per
+    sampled RHS timed; the full-step time is extrapolated by the total pole
+    count and the RHS count."""
     from oracle.models import RSW, Wave
     from oracle.rational import build_exp_approx
     from oracle.specelem import Mesh
+    if npoles_sample is None:
+        npoles_sample = 1 if cfg["n"] >= 32 else 2
     m = Mesh(cfg["n"], cfg["p"])
     model = RSW(m, cfg.get("f", 1.0)) if cfg["model"] == "rsw" else Wave(m, make_problem(cfg, m.x, m.y))
     ap = build_exp_approx(cfg["Lambda_tau"], cfg["delta"], verify=False)
-    u0 = initial_state(cfg["model"], m.x, m.y, cfg["seed"])
+    nr = min(nrhs_sample, cfg["nrhs"])
+    U = [initial_state(cfg["model"], m.x, m.y, cfg["seed"] + 10 * k) for k in range(nr)]
     P = len(ap["poles"])
-    idx = np.linspace(0, P - 1, npoles_sample).astype(int)
+    idx = np.linspace(0, P - 1, npoles_sample + 2).astype(int)[1:-1]
     solve_s = 0.0
     factor_s = 0.0
     for k in idx:
@@ -244,32 +306,71 @@ def oracle_sample(cfg, npoles_sample, seconds_budget=30.0):
         lu = model.factor(ap["poles"][k] / cfg["tau"])
         factor_s += time.perf_counter() - t0
         t0 = time.perf_counter()
-        _ = ap["res"][k] * model.resolvent(ap["poles"][k], cfg["tau"], u0, lu=lu)
+        for u0 in U:
+            _ = ap["res"][k] * model.resolvent(ap["poles"][k], cfg["tau"], u0, lu=lu)
         solve_s += time.perf_counter() - t0
-    step_s = solve_s / len(idx) * P
+        del lu
+    step_s = solve_s / (len(idx) * nr) * P * cfg["nrhs"]
     dof = 3 * m.N * cfg["nrhs"]
-    return {"value": dof / step_s, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{len(idx)} of {P} poles on the full {cfg['n']}x{cfg['n']}x{cfg['p']}^2 mesh, one "
-                      f"resolvent apply each (scipy splu factor untimed, {factor_s:.1f}s), step time "
-                      f"extrapolated x{P}/{len(idx)}",
+    return {"value": dof / step_s, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{len(idx)} of {P} poles x {nr} of {cfg['nrhs']} RHS on the full "
+                      f"{cfg['n']}x{cfg['n']}x{cfg['p']}^2 mesh, one resolvent apply each (scipy splu, "
+                      f"single-threaded; factor untimed, {factor_s:.1f}s), step time extrapolated "
+                      f"x{P}/{len(idx)} poles x{cfg['nrhs']}/{nr} RHS",
             "step_seconds": step_s}
+
+
+def bench_config(workload, cfg, poles, N):
+    """The `config` object of both arms (identical keys and values)."""
+    return {"workload": workload, "model": cfg["model"], "elements": f"{cfg['n']}x{cfg['n']}", "p": cfg["p"],
+            "Lambda_tau": cfg["Lambda_tau"], "tau": cfg["tau"], "delta": cfg["delta"], "nrhs": cfg["nrhs"],
+            "poles": poles, "dof": 3 * N * cfg["nrhs"], "nodes_per_field": N,
+            "baseline_nodes_per_field_convention": cfg["n"] ** 2 * cfg["p"] ** 2,
+            "l2": "operator store + work buffers exceed the 126 MB L2 (no flush needed)"}
+
+
+# The paper's own comparison (context, not the target): PAPER.md Tables 2 and 3
+# (PAPER.md:903-928, 1068-1089), all methods in Octave (PAPER.md:966-967), hardware
+# not stated; 12 x 12 elements of 16 x 16 nodes, one application of e^{1.5 L}.
+PAPER_CONTEXT = {
+    "source": "PAPER.md Table 2 (RSW, PAPER.md:903-928) and Table 3 (wave, PAPER.md:1068-1089); Octave "
+              "implementations (PAPER.md:966-967); hardware not stated",
+    "setup": "12x12 elements, 16x16 Chebyshev nodes each, one apply of exp(1.5 L), M = 376 terms",
+    "rsw_minutes": {"rational_apply": 4.39, "rational_precompute": 103.1, "rk4": 131.9, "chebyshev_deg12": 150.5},
+    "wave_minutes": {"rational_apply": 3.76, "rational_precompute": 113.4, "rk4": 63.9, "chebyshev_deg12": 57.5},
+    "rsw_rational_dof_steps_per_s": round(3 * 144 * 224 / (4.39 * 60), 1),
+}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle.rational import build_exp_approx
+    from oracle.specelem import Mesh
     t0 = time.perf_counter()
-    res = oracle_sample(cfg, npoles_sample=2)
+    res = oracle_sample(cfg)
+    poles = len(build_exp_approx(cfg["Lambda_tau"], cfg["delta"], verify=False)["poles"])
+    N = Mesh(cfg["n"], cfg["p"]).N
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["step_seconds"] * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": args.config, **{k: cfg[k] for k in ("model", "n", "p", "Lambda_tau", "tau",
-                                                                      "delta", "nrhs")}},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (fp64)",
+            "data": "synthetic", "config": bench_config(args.config, cfg, poles, N),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_s": round(time.perf_counter() - t0, 1)}
+            "paper_context": PAPER_CONTEXT, "wall_s": round(time.perf_counter() - t0, 1)}
     print(json.dumps(line), flush=True)
+
+
+def pernode_bytes_per_half_pole(cfg):
+    """Per-node store bytes of one half pole: dense leaf A_II^-1
+    (q^2 x q^2) and S_leaf (q^2 x 4q) per element, X / Y / S per merge-tree
+    node, dense periodic root (2nq)^2 - complex128."""
+    n, q = cfg["n"], cfg["p"] - 2
+    q2 = q * q
+    leaf = n * n * (q2 * q2 + q2 * 4 * q)
+    levs = sum(nd * (n3 * n3 + 2 * n3 * nx) for nd, n3, nx in tree_dims(n, q))
+    return 16 * (leaf + levs + (2 * n * q) ** 2)
 
 
 def run_ours(args, cfg):
@@ -294,12 +395,27 @@ def run_ours(args, cfg):
         xm, ym = api.mesh_coords(cfg["n"], cfg["p"])
         kappa = wave_speed_field(xm, ym, cfg["seed"])
     common = dict(f=cfg.get("f", 1.0), kappa=kappa, nrhs=cfg["nrhs"])
-    if world > 1:
-        # shard the half poles: rank r owns a contiguous range
+    nh_total = None
+    if world > 1 or args.shard is not None:
         tmp = api.setup(cfg["model"], cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, device=-1,
                         half_range=(0, 1), **common)
         nh_total = tmp.num_half_poles
         tmp.close()
+    shard = None
+    if args.shard is not None:
+        # one rank's share of a pole-sharded run on this GPU: the largest number of
+        # half poles whose per-node store fits (or the requested count)
+        if world > 1:
+            raise SystemExit("--shard is a single-GPU measurement")
+        per = pernode_bytes_per_half_pole(cfg)
+        free, total = torch.cuda.mem_get_info(dev)
+        fit = int((free - 24 * 2 ** 30) // per)
+        k = fit if args.shard == "auto" else min(int(args.shard), fit)
+        k = max(1, min(k, nh_total))
+        shard = (0, k)
+        h = api.setup(cfg["model"], cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, device=local,
+                      half_range=shard, **common)
+    elif world > 1:
         from paper_1402_5168_b200.parallel import half_range
         lo, hi = half_range(nh_total, rank, world)
         h = api.setup(cfg["model"], cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, device=local,
@@ -313,14 +429,16 @@ def run_ours(args, cfg):
     u0 = np.stack([initial_state(cfg["model"], x, y, cfg["seed"] + 10 * k) for k in range(cfg["nrhs"])])
     u = torch.from_numpy(u0).to(dev).contiguous()
     stream = torch.cuda.current_stream(dev)
-    e = torch.zeros(h.partial_len, dtype=torch.float64, device=dev) if world > 1 else None
+    sharded = world > 1 or shard is not None
+    e = torch.zeros(h.partial_len, dtype=torch.float64, device=dev) if sharded else None
 
     def one_step():
-        if world == 1:
+        if not sharded:
             api.apply(h, u, 1)
         else:
             api.step_partial(h, u, e)
-            dist.all_reduce(e)
+            if world > 1:
+                dist.all_reduce(e)
             api.step_finish(h, e, u)
 
     for _ in range(args.warmup):
@@ -363,7 +481,7 @@ def run_ours(args, cfg):
     # end-to-end through the public C ABI with HOST buffers: every step copies the
     # state in from pinned host memory, steps, and reads it back (rexp_apply host path)
     e2e = None
-    if world == 1:
+    if world == 1 and shard is None:
         uh = torch.from_numpy(u0.copy()).pin_memory()
         uh_np = uh.numpy()
         for _ in range(max(1, args.warmup)):
@@ -378,30 +496,41 @@ def run_ours(args, cfg):
                "timing": "host wall clock around K synchronous rexp_apply(host ptr, 1 step) calls"}
 
     pk = peaks()
-    roof = roofline_for(cfg, h, kt, args.steps, pk)
+    nh_here = (shard[1] - shard[0]) if shard else (hi - lo) if world > 1 else nh_total
+    roof = roofline_for(cfg, args.config, h, kt, args.steps, pk, ms / args.steps, nh_here)
     launches = sum(v[1] for v in kt.values())
+    conf = bench_config(args.config, cfg, h.num_poles, N)
+    conf["parallelism"] = (f"pole-sharded x{world}" if world > 1 else
+                           (f"one shard of a pole-sharded run: half poles [{shard[0]}, {shard[1]}) of {nh_total}"
+                            if shard else "single GPU"))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128 (fp64)", "data": "synthetic",
-            "config": {"workload": args.config, "model": cfg["model"], "elements": f"{cfg['n']}x{cfg['n']}",
-                       "p": cfg["p"], "Lambda_tau": cfg["Lambda_tau"], "tau": cfg["tau"], "delta": cfg["delta"],
-                       "nrhs": cfg["nrhs"], "poles": h.num_poles, "half_poles_total": nh_total,
-                       "dof": dof, "nodes_per_field": N,
-                       "baseline_nodes_per_field_convention": cfg["n"] ** 2 * cfg["p"] ** 2,
-                       "store": "shared" if cfg["model"] == "rsw" else "pernode",
-                       "leaf_solver": h.leaf_solver,
-                       "merge_kernels": h.stage_report,
-                       "store_bytes": h.store_bytes, "work_bytes": h.work_bytes,
-                       "l2": "operator store + work buffers exceed the 126 MB L2 (no flush needed)",
-                       "parallelism": f"pole-sharded x{world}" if world > 1 else "single GPU"},
+            "config": conf,
+            "impl_details": {"half_poles_total": nh_total, "half_poles_here": h.num_half_poles if shard is None
+                             else shard[1] - shard[0],
+                             "store": "shared" if cfg["model"] == "rsw" else "pernode",
+                             "leaf_solver": h.leaf_solver, "merge_kernels": h.stage_report,
+                             "store_bytes": h.store_bytes, "work_bytes": h.work_bytes},
             "roofline": roof,
             "kernel_ms": {k: round(v[0], 3) for k, v in kt.items()},
             "gpu_launches": launches, "e2e": e2e,
-            "clocks": clk.summary(), "setup_s": round(t_setup, 1), "finite": finite}
+            "clocks": clk.summary(), "setup_s": round(t_setup, 1), "finite": finite,
+            "paper_context": PAPER_CONTEXT}
+    if shard is not None:
+        per = pernode_bytes_per_half_pole(cfg)
+        line["shard"] = {
+            "half_poles": shard[1] - shard[0], "half_poles_total": nh_total,
+            "store_bytes_per_half_pole": per, "store_bytes_measured": h.store_bytes,
+            "full_store_bytes": per * nh_total,
+            "gpus_needed_for_full_store": math.ceil(per * nh_total / (torch.cuda.mem_get_info(dev)[1] - 24 * 2 ** 30)),
+            "value_meaning": "dof-steps/s of this shard's step (its half poles' pole sums + recovery); the full "
+                             "job on one GPU would run at value x half_poles / half_poles_total if it fit",
+            "full_job_equivalent": value * (shard[1] - shard[0]) / nh_total}
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and shard is None and not args.no_cpu_baseline:
             try:
-                cb = oracle_sample(cfg, npoles_sample=2)
+                cb = oracle_sample(cfg)
                 line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
             except Exception as ex:  # pragma: no cover
                 line["cpu_baseline"] = {"error": str(ex)}
@@ -419,6 +548,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default=None,
+                    help="'auto' or a half-pole count: time one rank's shard of a pole-sharded run on this GPU "
+                         "(configs whose store does not fit one B200: c2, c4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
