@@ -29,6 +29,7 @@
 #include "cgemm_launch.hpp"
 #include "cgemm_sym.cuh"
 #include "leaf_spec.cuh"
+#include "leaf_gemm.cuh"
 
 namespace rexp {
 namespace dev {
@@ -1227,6 +1228,49 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
             if ((rc = put(&d_Pi, Pi))) return rc;
         }
         store_bytes += static_cast<int64_t>(Dinv.size()) * 16;
+        // leaf GEMM coefficients (leaf_gemm.cuh header): orientation o, edge index r
+        //   UP   A_up[o][r][4 m + 2 s + c][(f, t)] = part c of (-/+ c1) c_mf Dinv_m(r, t) e_s[t]
+        //   DOWN A_dn[o][r][(k, t) | nE q + (k, s')][(m, s, c)]
+        //        = coef_s[t] (w.x | -w.y), w = -c2 d_mk Dinv_m(mode);   = (d_mk.x | -d_mk.y) if s = s'
+        lg_KP = nF * q <= 44 ? 44 : 48;
+        lg_MT = nE * q + 2 * nE <= 48 ? 6 : 7;
+        const size_t MR = 4 * static_cast<size_t>(nh), KP = lg_KP, MD = 8 * static_cast<size_t>(lg_MT);
+        std::vector<double> Aup(2 * q * MR * KP, 0.0), Adn(2 * q * MD * MR, 0.0);
+        auto dinv = [&](int m, int ip, int jp) {
+            const double2 v = Dinv[(static_cast<size_t>(m) * SP_T + ip) * SP_T + jp];
+            return cd(v.x, v.y);
+        };
+        for (int o = 0; o < 2; ++o)
+            for (int r = 0; r < q; ++r) {
+                double* U = Aup.data() + (static_cast<size_t>(o) * q + r) * MR * KP;
+                double* D = Adn.data() + (static_cast<size_t>(o) * q + r) * MD * MR;
+                for (int m = 0; m < nh; ++m)
+                    for (int sd = 0; sd < 2; ++sd) {
+                        const double sg = sd ? c1 : -c1;
+                        for (int f = 0; f < nF; ++f)
+                            for (int t = 0; t < q; ++t) {
+                                const cd z = sg * pt.cF[static_cast<size_t>(h0 + m) * nF + f] *
+                                             dinv(m, o ? t : r, o ? r : t) * E01[sd * SP_T + t];
+                                U[(4 * static_cast<size_t>(m) + 2 * sd + 0) * KP + f * q + t] = z.real();
+                                U[(4 * static_cast<size_t>(m) + 2 * sd + 1) * KP + f * q + t] = z.imag();
+                            }
+                        for (int k = 0; k < nE; ++k) {
+                            const cd d = pt.dE[static_cast<size_t>(h0 + m) * nE + k];
+                            for (int t = 0; t < q; ++t) {
+                                const int ip = o ? r : t, jp = o ? t : r;
+                                const cd w = -c2 * d * dinv(m, ip, jp);
+                                const double cf = A01[sd * SP_T + t];
+                                D[static_cast<size_t>(k * q + t) * MR + (2 * m + sd) * 2 + 0] = cf * w.real();
+                                D[static_cast<size_t>(k * q + t) * MR + (2 * m + sd) * 2 + 1] = -cf * w.imag();
+                            }
+                            D[static_cast<size_t>(nE * q + 2 * k + sd) * MR + (2 * m + sd) * 2 + 0] = d.real();
+                            D[static_cast<size_t>(nE * q + 2 * k + sd) * MR + (2 * m + sd) * 2 + 1] = -d.imag();
+                        }
+                    }
+            }
+        if ((rc = put(&d_Aup, Aup))) return rc;
+        if ((rc = put(&d_Adn, Adn))) return rc;
+        store_bytes += static_cast<int64_t>(Aup.size() + Adn.size()) * 8;
     }
     // operator store, filled by upload_ops (possibly in pole chunks)
     const size_t leaf_stored = shared ? 1 : static_cast<size_t>(nelem);
@@ -1324,15 +1368,15 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     if ((rc = walloc(&d_F, static_cast<size_t>(NI) * nF * R2, 8))) return rc;
     if (!fdm && (rc = walloc(&d_w, pc * NI * R2, 16))) return rc;
     if (fdm) {
-        // pole groups per leaf CTA: enough CTAs to fill the GPU (REXP_GROUPS overrides)
-        const long long ctas = static_cast<long long>(nelem) * nrhs;
+        // K slices of the leaf DOWN GEMM: enough CTAs for ~4 per SM over the lanes
+        // (REXP_GROUPS overrides); each slice owns a pole-sum partial slot
+        const long long ctas = 2LL * q * ((static_cast<long long>(nelem) * R2 + 127) / 128);
         const char* env = std::getenv("REXP_GROUPS");
-        // (lanes run concurrently: the target is shared between them)
-        ngroups = env ? std::atoi(env) : static_cast<int>((16LL * num_sms + ctas * nlanes - 1) / (ctas * nlanes));
-        ngroups = std::max(1, std::min(ngroups, chunk));
+        ngroups = env ? std::atoi(env) : static_cast<int>((4LL * num_sms + ctas * nlanes - 1) / (ctas * nlanes));
+        ngroups = std::max(1, std::min(ngroups, std::min(chunk, 32)));
         if ((rc = walloc(&d_G, static_cast<size_t>(nelem) * R2 * nF * q2, 8))) return rc;
         // partial slots [lane][group]
-        if ((rc = walloc(&d_Ehat, static_cast<size_t>(nlanes) * ngroups * nE * R2 * NI, 8))) return rc;
+        if ((rc = walloc(&d_Ehat, static_cast<size_t>(nlanes) * ngroups * 2 * nE * R2 * NI, 8))) return rc;
         if ((rc = walloc(&d_Eedge, static_cast<size_t>(nlanes) * ngroups * nE * R2 * NE, 8))) return rc;
     }
     lane_bufs.assign(nlanes, LaneBufs());
@@ -1591,10 +1635,10 @@ void DeviceStore::configure_kernels() {
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cgs_allow();
-    cudaFuncSetAttribute(k_leaf_spec_down<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_spec_up<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_spec_down<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_spec_up<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_gemm_up<44>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_gemm_up<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_gemm_down<6, 128, LGD_NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_leaf_gemm_down<7, 128, LGD_NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
@@ -1969,12 +2013,29 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     const int thr = ((q2 + 31) / 32) * 32;
     const int NBl = pick_nb(nelem, R2, shared);
     // ---- leaves up ----
-    SpecArgs sp = spec_args(m0, pc);
-    const dim3 sp_grid(static_cast<unsigned>(nelem * nrhs), static_cast<unsigned>(sp.ngroups));
+    LeafGemmArgs lg{};
     if (fdm) {
+        lg.q = q; lg.nelem = nelem; lg.R2 = R2; lg.ncol = nelem * R2; lg.nF = nF; lg.nE = nE;
+        lg.gB = d_leaf_gB; lg.own = d_leaf_own; lg.c1 = c1;
+        lg.Aup = d_Aup + static_cast<size_t>(4) * m0 * lg_KP;
+        lg.aup_os = static_cast<long long>(4) * nh * lg_KP;
+        lg.Mrows = 4 * pc;
+        lg.G = d_G; lg.h = d_h[0]; lg.hps = hstride;
+        lg.lda = 4 * nh;
+        lg.Adn = d_Adn + static_cast<size_t>(4) * m0;
+        lg.adn_os = static_cast<long long>(8) * lg_MT * lg.lda;
+        lg.Kdn = 4 * pc; lg.ksplit = ngroups;
+        lg.edge = d_edge; lg.NE = NE;
+        lg.ehat_ss = static_cast<long long>(nE) * q2 * nelem * R2;
+        lg.eedge_ss = static_cast<long long>(nE) * NE * R2;
+        lg.Ehat = d_Ehat + static_cast<size_t>(cur_lane) * ngroups * 2 * lg.ehat_ss;
+        lg.Eedge = d_Eedge + static_cast<size_t>(cur_lane) * ngroups * lg.eedge_ss;
+        lg.accumulate = m0 > lane_bufs[cur_lane].m0 ? 1 : 0;
+        const dim3 gu(static_cast<unsigned>((4 * pc + LGU_BM - 1) / LGU_BM),
+                      static_cast<unsigned>((lg.ncol + LGU_BN - 1) / LGU_BN), static_cast<unsigned>(2 * q));
         tbeg(s);
-        if (q == 14) k_leaf_spec_up<14><<<sp_grid, SP_THREADS, sp_up_smem(), s>>>(sp);
-        else k_leaf_spec_up<0><<<sp_grid, SP_THREADS, sp_up_smem(), s>>>(sp);
+        if (lg_KP == 44) k_leaf_gemm_up<44><<<gu, 32 * LGU_WM * LGU_WN, lg_up_smem<44>(), s>>>(lg);
+        else k_leaf_gemm_up<48><<<gu, 32 * LGU_WM * LGU_WN, lg_up_smem<48>(), s>>>(lg);
         tend(T_LEAF_UP, s);
     } else if (shared) {
         CgemmArgs a{};
@@ -2026,9 +2087,10 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     }
     // ---- leaves down ----
     if (fdm) {
+        const dim3 gd(static_cast<unsigned>((lg.ncol + 127) / 128), static_cast<unsigned>(2 * q * ngroups));
         tbeg(s);
-        if (q == 14) k_leaf_spec_down<14><<<sp_grid, SP_THREADS, sp_down_smem(), s>>>(sp);
-        else k_leaf_spec_down<0><<<sp_grid, SP_THREADS, sp_down_smem(), s>>>(sp);
+        if (lg_MT == 6) k_leaf_gemm_down<6, 128, LGD_NST><<<gd, 128, lg_dn_smem<6, 128, LGD_NST>(), s>>>(lg);
+        else k_leaf_gemm_down<7, 128, LGD_NST><<<gd, 128, lg_dn_smem<7, 128, LGD_NST>(), s>>>(lg);
         tend(T_LEAF_DOWN, s);
     } else if (shared) {
         CgemmArgs a{};
@@ -2072,7 +2134,7 @@ SpecArgs DeviceStore::spec_args(int m0, int pc) const {
     sp.h = d_h[0]; sp.hps = hstride;
     sp.edge = d_edge; sp.NE = NE; sp.gB = d_leaf_gB; sp.own = d_leaf_own;
     // this lane's partial slots (k_spec_back sums every lane's)
-    sp.Ehat = d_Ehat + static_cast<size_t>(cur_lane) * ngroups * nE * R2 * NI;
+    sp.Ehat = d_Ehat + static_cast<size_t>(cur_lane) * ngroups * 2 * nE * R2 * NI;
     sp.Eedge = d_Eedge + static_cast<size_t>(cur_lane) * ngroups * nE * R2 * NE;
     sp.Pi = d_Pi; sp.E = nullptr; sp.N = N;
     return sp;
@@ -2131,7 +2193,7 @@ int DeviceStore::solve_sum(const double* d_state, double* d_E_out, cudaStream_t 
     use_lane(0);
     if (fdm) {
         SpecArgs sp = spec_args(0, chunk);
-        sp.ngroups = nlanes * std::min(ngroups, chunk);   // every lane's slots
+        sp.ngroups = nlanes * ngroups;   // every lane's K-slice slots (x 2 orientations for E^)
         sp.Ehat = d_Ehat;
         sp.Eedge = d_Eedge;
         sp.E = d_E_out;

@@ -121,289 +121,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_pre_fused(SpecArgs a) {
         const int f = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
         double sum = 0.0;
         for (int j = 0; j < q; ++j) sum = fma(ts[f][j * q + ip], vis[jp * (SP_T + 1) + j], sum);
-        a.G[(((size_t)leaf * a.R2 + r2) * a.nF + f) * q2 + mode] = sum;
-    }
-}
-
-// the thread's spectral RHS coefficients G_f[mode] for both real parts of RHS k
-__device__ __forceinline__ void sp_load_g(const SpecArgs& a, int leaf, int k, int mode, double (&g)[2][3]) {
-    const int q2 = a.q * a.q;
-#pragma unroll
-    for (int part = 0; part < 2; ++part)
-#pragma unroll
-        for (int f = 0; f < 3; ++f)
-            g[part][f] = (f < a.nF) ? a.G[(((size_t)leaf * a.R2 + 2 * k + part) * a.nF + f) * q2 + mode] : 0.0;
-}
-
-// --------------------------------------------------------------------------
-// k_leaf_spec_up: h_m = N_I A_m^-1 f_m in the edge basis   (grid: nelem * nrhs, ngroups)
-// Per batch of SP_PB half poles: thread (i', j') forms W = Dinv_m .* sum_f c_mf G_f;
-// then task (pp, part, row|col, r) forms y_s[r] = sum_j' W[r][j'] e_s[j'] (rows) or
-// z_s[r] = sum_i' W[i'][r] e_s[i'] (columns), s = 0, 1, and writes the flux
-//   bottom -c1 y0, top +c1 y1, left -c1 z0, right +c1 z1   (edge basis: no V).
-// --------------------------------------------------------------------------
-__device__ __forceinline__ void sp_fetch_dinv(const SpecArgs& a, int mb, int nbat, double2* dst);
-
-constexpr size_t sp_up_smem() {
-    return (2 * (size_t)SP_PB * SP_T * SP_T + (size_t)SP_PB * 2 * SP_T * SP_LW + 2 * SP_PB * 4) * sizeof(double2) +
-           2 * SP_T * sizeof(double);
-}
-
-// QT: compile-time q (0 = runtime a.q); q = 14 (p = 16) is instantiated so the
-// per-pole loops have constant trip counts
-template <int QT>
-__global__ void __launch_bounds__(SP_THREADS) k_leaf_spec_up(SpecArgs a) {
-    extern __shared__ double2 usm[];
-    double2* Ds = usm;                                   // [2][SP_PB][256] Dinv rows (cp.async, one batch ahead)
-    double2* Ws = Ds + 2 * SP_PB * SP_T * SP_T;          // [SP_PB][2][SP_T * SP_LW] W[i'][j'] at j'*SP_LW + i'
-    double2* cfs = Ws + SP_PB * 2 * SP_T * SP_LW;        // [2][SP_PB][4] c_mf
-    double* es = reinterpret_cast<double*>(cfs + 2 * SP_PB * 4);
-    const int q = QT ? QT : a.q, nbnd = 4 * q, t = threadIdx.x;
-    const int nrhs = a.R2 / 2;
-    const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
-    int m0, m1;
-    sp_group_range(a, blockIdx.y, m0, m1);
-    if (t < 2 * SP_T) es[t] = a.E01[t];
-    const int ip = t & 15, jp = t >> 4;
-    const bool act = ip < q && jp < q;
-    const int wpos = jp * SP_LW + ip;
-    double g[2][3];
-    if (act) sp_load_g(a, leaf, k, jp * q + ip, g);
-    const int cf_pp = t >> 2, cf_f = t & 3;              // c_mf staging task (t < 4 SP_PB)
-    {
-        const int nb0 = min(SP_PB, m1 - m0);
-        sp_fetch_dinv(a, m0, nb0, Ds);
-        if (t < 4 * SP_PB)
-            cfs[t] = (cf_pp < nb0 && cf_f < a.nF) ? a.cF[(size_t)(m0 + cf_pp) * a.nF + cf_f] : make_double2(0.0, 0.0);
-        cp_async_wait_all();
-    }
-    __syncthreads();
-    int buf = 0;
-    for (int mb = m0; mb < m1; mb += SP_PB, buf ^= 1) {
-        const int nbat = min(SP_PB, m1 - mb);
-        const bool more = mb + SP_PB < m1;
-        double2 pcf = make_double2(0.0, 0.0);
-        if (more) {
-            const int nbn = min(SP_PB, m1 - mb - SP_PB);
-            sp_fetch_dinv(a, mb + SP_PB, nbn, Ds + (buf ^ 1) * SP_PB * SP_T * SP_T);
-            if (t < 4 * SP_PB && cf_pp < nbn && cf_f < a.nF) pcf = a.cF[(size_t)(mb + SP_PB + cf_pp) * a.nF + cf_f];
-        }
-        const double2* Db = Ds + buf * SP_PB * SP_T * SP_T;
-        const double2* cb = cfs + buf * SP_PB * 4;
-        // W = Dinv_m .* sum_f c_mf G_f
-        if (act) {
-#pragma unroll
-            for (int pp = 0; pp < SP_PB; ++pp) {
-                if (pp < nbat) {
-                    const double2 c0 = cb[pp * 4 + 0], c1v = cb[pp * 4 + 1], c2v = cb[pp * 4 + 2];
-                    const double2 d = Db[pp * SP_T * SP_T + t];
-#pragma unroll
-                    for (int part = 0; part < 2; ++part) {
-                        const double sx = c0.x * g[part][0] + c1v.x * g[part][1] + c2v.x * g[part][2];
-                        const double sy = c0.y * g[part][0] + c1v.y * g[part][1] + c2v.y * g[part][2];
-                        Ws[(pp * 2 + part) * SP_T * SP_LW + wpos] = make_double2(sx * d.x - sy * d.y, sx * d.y + sy * d.x);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        for (int task = t; task < nbat * 64; task += blockDim.x) {
-            const int pp = task >> 6, part = (task >> 5) & 1, col = (task >> 4) & 1, r = task & 15;
-            if (r >= q) continue;
-            const double2* W = Ws + (pp * 2 + part) * SP_T * SP_LW;
-            const int base = col ? r * SP_LW : r, step = col ? 1 : SP_LW;
-            double s0x = 0.0, s0y = 0.0, s1x = 0.0, s1y = 0.0;
-            for (int c = 0; c < q; ++c) {
-                const double2 w = W[base + c * step];
-                const double e0 = es[c], e1 = es[SP_T + c];
-                s0x = fma(w.x, e0, s0x); s0y = fma(w.y, e0, s0y);
-                s1x = fma(w.x, e1, s1x); s1y = fma(w.y, e1, s1y);
-            }
-            double2* hb = a.h + ((size_t)(mb + pp) * a.hps + (size_t)leaf * nbnd) * a.R2 + 2 * k + part;
-            const int side0 = col ? 3 : 0, side1 = col ? 1 : 2;   // (bottom, top) or (left, right)
-            hb[(size_t)(side0 * q + r) * a.R2] = make_double2(-a.c1 * s0x, -a.c1 * s0y);
-            hb[(size_t)(side1 * q + r) * a.R2] = make_double2(a.c1 * s1x, a.c1 * s1y);
-        }
-        // stage the next batch's c_mf; Ws / Ds[buf] are rewritten after the barrier
-        if (more && t < 4 * SP_PB) cfs[(buf ^ 1) * SP_PB * 4 + t] = pcf;
-        cp_async_wait_all();
-        __syncthreads();
-    }
-}
-
-// --------------------------------------------------------------------------
-// k_leaf_spec_down: interior pole sums, boundary-driven part
-//   W_m = Dinv_m .* V^-1 (f_m - A_IB u_B,m) V^-T  and  E^_k = sum_m Re(d_mk W_m).
-// The f_m part is pole-independent up to a per-mode weight,
-//   sum_m Re(d_mk c_mf Dinv_m) =: Pi_kf   (setup, device.cu),
-// and is added once per step in k_spec_back; per pole only
-//   E^_k += Re((-c2 d_mk) Dinv_m .* b_m),  b_m = a0^ ul^T + a1^ ur^T + ub^ a0^T + ut^ a1^T
-// remains (u^_side: the edge values, already in the edge basis), plus the
-// (edge-basis) pole sums of the edge segments this leaf owns.
-// Per batch of SP_PB half poles the boundary values (registers) and the Dinv
-// rows (cp.async) of the NEXT batch are in flight while this batch computes.
-//   (grid: nelem * nrhs, ngroups; dynamic shared memory sp_down_smem())
-// --------------------------------------------------------------------------
-constexpr int SP_UBN = SP_PB * 2 * SP_NB;              // boundary values staged per batch
-constexpr int SP_UBR = (SP_UBN + SP_THREADS - 1) / SP_THREADS;
-
-// staged layout [pp][part][b]: consecutive modes read consecutive banks
-__device__ __forceinline__ void sp_fetch_ub(const SpecArgs& a, const int* gb, int k, int mb, int nbat, int nbnd,
-                                            double2 (&r)[SP_UBR]) {
-#pragma unroll
-    for (int u = 0; u < SP_UBR; ++u) {
-        const int task = threadIdx.x + u * SP_THREADS;   // (pp, b, part), part fastest: coalesced reads
-        const int pp = task / (2 * nbnd), rem = task % (2 * nbnd);
-        r[u] = make_double2(0.0, 0.0);
-        if (pp < nbat)
-            r[u] = a.edge[((size_t)(mb + pp) * a.NE + gb[rem >> 1]) * a.R2 + 2 * k + (rem & 1)];
-    }
-}
-__device__ __forceinline__ void sp_stage_ub(const double2 (&r)[SP_UBR], int nbnd, double2* dst) {
-#pragma unroll
-    for (int u = 0; u < SP_UBR; ++u) {
-        const int task = threadIdx.x + u * SP_THREADS;
-        const int pp = task / (2 * nbnd), rem = task % (2 * nbnd);
-        if (pp < SP_PB) dst[(pp * 2 + (rem & 1)) * SP_NB + (rem >> 1)] = r[u];
-    }
-}
-
-// Dinv rows of a batch: SP_PB x 256 complex, one 16-byte cp.async per thread per pole
-__device__ __forceinline__ void sp_fetch_dinv(const SpecArgs& a, int mb, int nbat, double2* dst) {
-    for (int pp = 0; pp < nbat; ++pp)
-        cp_async16(dst + pp * SP_T * SP_T + threadIdx.x, a.Dinv + (size_t)(mb + pp) * SP_T * SP_T + threadIdx.x);
-    cp_async_commit();
-}
-
-constexpr size_t sp_down_smem() {
-    return (2 * (size_t)SP_UBN + 2 * (size_t)SP_PB * SP_T * SP_T + 2 * SP_PB * 4) * sizeof(double2) +
-           2 * SP_T * sizeof(double);
-}
-
-template <int QT>
-__global__ void __launch_bounds__(SP_THREADS, 3) k_leaf_spec_down(SpecArgs a) {
-    extern __shared__ double2 dsm[];
-    double2* UBs = dsm;                                  // [2][SP_PB][2][SP_NB] edge-basis boundary values
-    double2* Ds = UBs + 2 * SP_UBN;                      // [2][SP_PB][256] Dinv rows
-    double2* dEs = Ds + 2 * SP_PB * SP_T * SP_T;         // [2][SP_PB][4]   d_mk
-    double* as = reinterpret_cast<double*>(dEs + 2 * SP_PB * 4);
-    const int q = QT ? QT : a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
-    const int nrhs = a.R2 / 2;
-    const int leaf = blockIdx.x / nrhs, k = blockIdx.x % nrhs;
-    const int grp = blockIdx.y;
-    int m0, m1;
-    sp_group_range(a, grp, m0, m1);
-    if (t < 2 * SP_T) as[t] = a.A01[t];
-    const int ip = t & 15, jp = t >> 4;
-    const bool act = ip < q && jp < q;
-    double Eacc[2][3];
-#pragma unroll
-    for (int part = 0; part < 2; ++part)
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk) Eacc[part][kk] = 0.0;
-    const size_t NIs = (size_t)a.nelem * q2;
-    double* Eout = a.Ehat + (size_t)grp * a.nE * a.R2 * NIs + (size_t)leaf * q2 + (jp * q + ip);
-    if (act && a.accumulate) {
-#pragma unroll
-        for (int part = 0; part < 2; ++part)
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk)
-                if (kk < a.nE) Eacc[part][kk] = Eout[((size_t)kk * a.R2 + 2 * k + part) * NIs];
-    }
-    const int* gb = a.gB + (size_t)leaf * nbnd;
-    // edge pole sums: thread t < 2*nbnd owns (b, part) = (t >> 1, t & 1) if the leaf owns node b
-    const int e_b = t >> 1, e_part = t & 1;
-    const bool eact = t < 2 * nbnd && a.own[(size_t)leaf * nbnd + e_b];
-    double Eg[3] = {0.0, 0.0, 0.0};
-    double* Eeout = nullptr;
-    if (eact) {
-        Eeout = a.Eedge + (size_t)grp * a.nE * a.R2 * a.NE + (size_t)(2 * k + e_part) * a.NE + gb[e_b];
-        if (a.accumulate) {
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk)
-                if (kk < a.nE) Eg[kk] = Eeout[(size_t)kk * a.R2 * a.NE];
-        }
-    }
-    // prologue: batch 0 staged
-    double2 pre[SP_UBR];
-    double2 pde = make_double2(0.0, 0.0);
-    const int de_pp = t >> 2, de_k = t & 3;              // d_mk staging task (t < 4 SP_PB)
-    {
-        const int nb0 = min(SP_PB, m1 - m0);
-        sp_fetch_ub(a, gb, k, m0, nb0, nbnd, pre);
-        sp_fetch_dinv(a, m0, nb0, Ds);
-        if (t < 4 * SP_PB && de_pp < nb0 && de_k < a.nE) pde = a.dE[(size_t)(m0 + de_pp) * a.nE + de_k];
-        sp_stage_ub(pre, nbnd, UBs);
-        if (t < 4 * SP_PB) dEs[t] = pde;
-        cp_async_wait_all();
-    }
-    __syncthreads();
-    const double mc2 = -a.c2;
-    int buf = 0;
-    for (int mb = m0; mb < m1; mb += SP_PB, buf ^= 1) {
-        const int nbat = min(SP_PB, m1 - mb);
-        const bool more = mb + SP_PB < m1;
-        if (more) {
-            const int nbn = min(SP_PB, m1 - mb - SP_PB);
-            sp_fetch_ub(a, gb, k, mb + SP_PB, nbn, nbnd, pre);
-            sp_fetch_dinv(a, mb + SP_PB, nbn, Ds + (buf ^ 1) * SP_PB * SP_T * SP_T);
-            pde = make_double2(0.0, 0.0);
-            if (t < 4 * SP_PB && de_pp < nbn && de_k < a.nE) pde = a.dE[(size_t)(mb + SP_PB + de_pp) * a.nE + de_k];
-        }
-        const double2* ub = UBs + buf * SP_UBN;
-        const double2* Db = Ds + buf * SP_PB * SP_T * SP_T;
-        const double2* dEb = dEs + buf * SP_PB * 4;
-        if (act) {
-            const double a0i = as[ip], a1i = as[SP_T + ip], a0j = as[jp], a1j = as[SP_T + jp];
-#pragma unroll
-            for (int pp = 0; pp < SP_PB; ++pp) {
-                if (pp < nbat) {
-                    const double2 d = Db[pp * SP_T * SP_T + t];
-                    const double2 d0 = dEb[pp * 4 + 0], d1 = dEb[pp * 4 + 1], d2 = dEb[pp * 4 + 2];
-#pragma unroll
-                    for (int part = 0; part < 2; ++part) {
-                        const double2* U = ub + (pp * 2 + part) * SP_NB;   // [bottom | right | top | left]
-                        const double2 ubv = U[ip], ur = U[q + jp], ut = U[2 * q + ip], ul = U[3 * q + jp];
-                        const double bx = a0i * ul.x + a1i * ur.x + ubv.x * a0j + ut.x * a1j;
-                        const double by = a0i * ul.y + a1i * ur.y + ubv.y * a0j + ut.y * a1j;
-                        // t = -c2 Dinv b
-                        const double tx = mc2 * (bx * d.x - by * d.y), ty = mc2 * (bx * d.y + by * d.x);
-                        Eacc[part][0] += d0.x * tx - d0.y * ty;
-                        Eacc[part][1] += d1.x * tx - d1.y * ty;
-                        Eacc[part][2] += d2.x * tx - d2.y * ty;
-                    }
-                }
-            }
-        }
-        if (eact) {
-            for (int pp = 0; pp < nbat; ++pp) {
-                const double2 u = ub[(pp * 2 + e_part) * SP_NB + e_b];
-#pragma unroll
-                for (int kk = 0; kk < 3; ++kk) {
-                    const double2 de = dEb[pp * 4 + kk];
-                    Eg[kk] += de.x * u.x - de.y * u.y;
-                }
-            }
-        }
-        // stage the prefetched batch into the other buffers (read after the barrier)
-        if (more) {
-            sp_stage_ub(pre, nbnd, UBs + (buf ^ 1) * SP_UBN);
-            if (t < 4 * SP_PB) dEs[(buf ^ 1) * SP_PB * 4 + t] = pde;
-        }
-        cp_async_wait_all();
-        __syncthreads();
-    }
-    if (act) {
-#pragma unroll
-        for (int part = 0; part < 2; ++part)
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk)
-                if (kk < a.nE) Eout[((size_t)kk * a.R2 + 2 * k + part) * NIs] = Eacc[part][kk];
-    }
-    if (eact) {
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk)
-            if (kk < a.nE) Eeout[(size_t)kk * a.R2 * a.NE] = Eg[kk];
+        a.G[((size_t)(f * q + ip) * q + jp) * ((size_t)a.nelem * a.R2) + (size_t)leaf * a.R2 + r2] = sum;
     }
 }
 
@@ -418,17 +136,17 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
     __shared__ double eb[3][SP_NB];
     const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
     const int leaf = blockIdx.x / a.R2, r2 = blockIdx.x % a.R2;
-    const size_t NIs = (size_t)a.nelem * q2;
+    const size_t ncol = (size_t)a.nelem * a.R2, col = blockIdx.x;   // column = leaf * R2 + r2
     for (int e = t; e < SP_T * SP_T; e += blockDim.x) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
     __syncthreads();
     for (int e = t; e < a.nE * q2; e += blockDim.x) {
         const int kk = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
-        const double* src = a.Ehat + ((size_t)kk * a.R2 + r2) * NIs + (size_t)leaf * q2 + mode;
+        const double* src = a.Ehat + ((size_t)(kk * q + ip) * q + jp) * ncol + col;
         double s = 0.0;
-        for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.R2 * NIs];
+        for (int gi = 0; gi < 2 * a.ngroups; ++gi) s += src[(size_t)gi * a.nE * q2 * ncol];
         // pole-independent RHS part: sum_f Pi_kf G_f
-        const double* G = a.G + ((size_t)leaf * a.R2 + r2) * a.nF * q2 + mode;
-        for (int f = 0; f < a.nF; ++f) s += a.Pi[((size_t)kk * a.nF + f) * SP_T * SP_T + ip * SP_T + jp] * G[(size_t)f * q2];
+        const double* G = a.G + ((size_t)ip * q + jp) * ncol + col;
+        for (int f = 0; f < a.nF; ++f) s += a.Pi[((size_t)kk * a.nF + f) * SP_T * SP_T + ip * SP_T + jp] * G[(size_t)f * q2 * ncol];
         es[kk][mode] = s;   // E^[i'][j'] at j'*q + i'
     }
     // owned edge segments: sum over groups (into shared memory), then back from
@@ -437,8 +155,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
         const int kk = e / nbnd, b = e % nbnd;
         double s = 0.0;
         if (a.own[(size_t)leaf * nbnd + b]) {
-            const double* src = a.Eedge + ((size_t)kk * a.R2 + r2) * a.NE + a.gB[(size_t)leaf * nbnd + b];
-            for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.R2 * a.NE];
+            const double* src = a.Eedge + ((size_t)kk * a.NE + a.gB[(size_t)leaf * nbnd + b]) * a.R2 + r2;
+            for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.NE * a.R2];
         }
         eb[kk][b] = s;
     }

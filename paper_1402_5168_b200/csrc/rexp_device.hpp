@@ -112,7 +112,9 @@ class DeviceStore {
     double *d_V = nullptr, *d_Vinv = nullptr, *d_D2 = nullptr, *d_E01 = nullptr, *d_A01 = nullptr;
     double *d_G = nullptr, *d_Ehat = nullptr, *d_Eedge = nullptr, *d_Pi = nullptr;   // spectral RHS fields, pole-sum partials
     int* d_leaf_own = nullptr;                  // [nelem][4q] edge-node ownership for the pole sums
-    int ngroups = 1;                            // pole groups per leaf CTA (spectral path)
+    double *d_Aup = nullptr, *d_Adn = nullptr;  // leaf GEMM coefficients (leaf_gemm.cuh), [2q][..]
+    int lg_KP = 44, lg_MT = 6;                  // their K padding (UP) / row tiles (DOWN)
+    int ngroups = 1;                            // K slices of the leaf DOWN GEMM = pole-sum partial slots per lane
     int chunk = 1;             // half poles per work-buffer chunk
     int num_sms = 148;
     size_t pp_Ainv = 0, pp_Sleaf = 0, pp_Xroot = 0;
