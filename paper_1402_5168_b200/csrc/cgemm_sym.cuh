@@ -49,10 +49,42 @@ __device__ __forceinline__ void cgs_fetch1(const CgemmSymArgs& s, int m, int pos
     }
 }
 
-// epilogue: half row rr -> rows oA[rr] (y_A) and oB[rr] (y_B)
+// additive epilogue terms of the thread's outputs (UP-Y: child h[ext], DOWN: w3),
+// fetched before the K loop so their latency overlaps the operand loads (PF)
 template <int R2T, int MODE, int MT>
+__device__ __forceinline__ void cgs_prefetch_add(const CgemmSymArgs& s, int m, int row0, int col0, int mrow0,
+                                                 int warp, int g, int t4, double2 (&pre)[MT][2][2]) {
+    const CgemmArgs& a = s.g;
+    const int R2 = R2T ? R2T : a.R2;
+    const int hr = a.rows, ncols = a.nodes * R2;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            pre[i][j][0] = pre[i][j][1] = make_double2(0.0, 0.0);
+            const int rr = row0 + mrow0 + i * 8 + g;
+            const int col = col0 + warp * 8 + 2 * t4 + j;
+            if (rr >= hr || col >= ncols) continue;
+            const int node = col / R2, r2 = col % R2;
+            const int ra = s.oA[rr], rbw = s.oB[rr];
+            if (MODE == CG_UPY) {
+                const int base = cg_child_base(a, node);
+                pre[i][j][0] = a.add[((size_t)m * a.add_ps + base + a.ai0[ra]) * R2 + r2];
+                pre[i][j][1] = a.add[((size_t)m * a.add_ps + base + a.ai0[rbw]) * R2 + r2];
+            } else if (MODE == CG_DOWN) {
+                const double2* w3 = a.add + (size_t)m * a.add_ps * R2;
+                pre[i][j][0] = w3[((size_t)node * s.n3 + ra) * R2 + r2];
+                pre[i][j][1] = w3[((size_t)node * s.n3 + rbw) * R2 + r2];
+            }
+        }
+}
+
+// epilogue: half row rr -> rows oA[rr] (y_A) and oB[rr] (y_B); PF: the additive
+// terms were prefetched into pre
+template <int R2T, int MODE, int MT, bool PF = false>
 __device__ __forceinline__ void cgs_epilogue(const CgemmSymArgs& s, int m, int row0, int col0, int mrow0, int warp,
-                                             int g, int t4, const double (&acc)[2][MT][4]) {
+                                             int g, int t4, const double (&acc)[2][MT][4],
+                                             const double2 (*pre)[2][2] = nullptr) {
     const CgemmArgs& a = s.g;
     const int R2 = R2T ? R2T : a.R2;
     const int hr = a.rows, ncols = a.nodes * R2;
@@ -76,15 +108,15 @@ __device__ __forceinline__ void cgs_epilogue(const CgemmSymArgs& s, int m, int r
                 dst[((size_t)node * s.n3 + rbw) * R2 + r2] = yB;
             } else if (MODE == CG_UPY) {
                 const int base = cg_child_base(a, node);
-                const double2 ea = a.add[((size_t)m * a.add_ps + base + a.ai0[ra]) * R2 + r2];
-                const double2 eb = a.add[((size_t)m * a.add_ps + base + a.ai0[rbw]) * R2 + r2];
+                const double2 ea = PF ? pre[i][j][0] : a.add[((size_t)m * a.add_ps + base + a.ai0[ra]) * R2 + r2];
+                const double2 eb = PF ? pre[i][j][1] : a.add[((size_t)m * a.add_ps + base + a.ai0[rbw]) * R2 + r2];
                 double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
                 dst[((size_t)node * s.next + ra) * R2 + r2] = make_double2(yA.x + ea.x, yA.y + ea.y);
                 dst[((size_t)node * s.next + rbw) * R2 + r2] = make_double2(yB.x + eb.x, yB.y + eb.y);
             } else {   // DOWN: u3 = y + w3, scattered to the edge array
                 const double2* w3 = a.add + (size_t)m * a.add_ps * R2;
-                const double2 wa = w3[((size_t)node * s.n3 + ra) * R2 + r2];
-                const double2 wb = w3[((size_t)node * s.n3 + rbw) * R2 + r2];
+                const double2 wa = PF ? pre[i][j][0] : w3[((size_t)node * s.n3 + ra) * R2 + r2];
+                const double2 wb = PF ? pre[i][j][1] : w3[((size_t)node * s.n3 + rbw) * R2 + r2];
                 a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + ra]) * R2 + r2] =
                     make_double2(yA.x + wa.x, yA.y + wa.y);
                 a.dst[((size_t)m * a.dst_ps + a.so0[(size_t)node * s.n3 + rbw]) * R2 + r2] =
@@ -94,9 +126,14 @@ __device__ __forceinline__ void cgs_epilogue(const CgemmSymArgs& s, int m, int r
     }
 }
 
+// NST: 2 = B+- formed through registers (double-buffered); 3 = cp.async ring of
+// 3 stages; 12 / 11 = cp.async ring of 2 / 1 stage(s) (smaller footprint: more
+// CTAs per SM for the short-K, latency-bound low levels)
+template <int NST>
+__host__ __device__ constexpr int cgs_ring() { return NST >= 10 ? NST - 10 : NST; }
 template <int MT, int WN, int BK, int WM = 1, int NST = 2>
-constexpr size_t cgemm_sym_smem_bytes() {
-    return (size_t)NST * 2 * BK * ((8 * MT * WM + 2) + (8 * WN + 2)) * sizeof(double2);
+__host__ __device__ constexpr size_t cgemm_sym_smem_bytes() {
+    return (size_t)cgs_ring<NST>() * 2 * BK * ((8 * MT * WM + 2) + (8 * WN + 2)) * sizeof(double2);
 }
 
 // gathered source address of x at full input position pos (UP-Y, DOWN: one 16-byte value)
@@ -111,7 +148,7 @@ __device__ __forceinline__ const double2* cgs_src(const CgemmSymArgs& s, int m, 
 // NST = 2: B+- formed through registers.  NST = 3 (UP-Y / DOWN): both halves of A
 // and the raw x_A, x_B tiles by cp.async into a 3-stage ring; B+- formed in the
 // compute loop (b+- = x_A +- s x_B).
-template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int NST = 2>
+template <int MT, int WN, int BK, int R2T, int MODE, int WM = 1, int NST = 2, bool PF = false>
 __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
     const CgemmArgs& a = s.g;
     constexpr int BM = 8 * MT * WM, BN = 8 * WN, NT = 32 * WN * WM;
@@ -134,9 +171,10 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
     const double2* Am = Ap + (size_t)hr * hk;            // M-
 
     if constexpr (NST >= 3 && (MODE == CG_UPY || MODE == CG_DOWN)) {
-        // ring of NST stages: [stage][half] A tiles, then [stage][A|B] raw x tiles
+        // ring of RS stages: [stage][half] A tiles, then [stage][A|B] raw x tiles
+        constexpr int RS = cgs_ring<NST>();
         auto AsN = [&](int st, int hf) { return sm + (st * 2 + hf) * BK * LDA; };
-        auto XsN = [&](int st, int ab) { return sm + NST * 2 * BK * LDA + (st * 2 + ab) * BK * LDB; };
+        auto XsN = [&](int st, int ab) { return sm + RS * 2 * BK * LDA + (st * 2 + ab) * BK * LDB; };
         auto issue = [&](int st, int k0) {
             for (int e = tid; e < 2 * BK * BM; e += NT) {
                 const int hf = e / (BK * BM), ee = e % (BK * BM);
@@ -169,17 +207,26 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
             }
         const int nch = (hk + BK - 1) / BK;
 #pragma unroll
-        for (int st = 0; st < NST - 1; ++st) {
+        for (int st = 0; st < RS - 1; ++st) {
             if (st < nch) issue(st, st * BK);
             else cp_async_commit();
         }
+        double2 pre3[PF ? MT : 1][2][2];
+        if constexpr (PF) cgs_prefetch_add<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, pre3);
         for (int ch = 0; ch < nch; ++ch) {
-            cp_async_wait_group<NST - 2>();
-            __syncthreads();
-            const int nx = ch + NST - 1;
-            if (nx < nch) issue(nx % NST, nx * BK);
-            else cp_async_commit();
-            const int st = ch % NST;
+            if constexpr (RS == 1) {
+                if (ch > 0) __syncthreads();    // everyone is done with the single stage
+                issue(0, ch * BK);
+                cp_async_wait_all();
+                __syncthreads();
+            } else {
+                cp_async_wait_group<(RS >= 2 ? RS - 2 : 0)>();
+                __syncthreads();
+                const int nx = ch + RS - 1;
+                if (nx < nch) issue(nx % RS, nx * BK);
+                else cp_async_commit();
+            }
+            const int st = RS == 1 ? 0 : ch % RS;
             const double2* XA = XsN(st, 0);
             const double2* XB = XsN(st, 1);
 #pragma unroll
@@ -224,7 +271,7 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
 #pragma unroll
             for (int i = 0; i < MT; ++i) cmul3_finish(acc3[hf][i], q3[hf][i]);
 #endif
-        cgs_epilogue<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, acc3);
+        cgs_epilogue<R2T, MODE, MT, PF>(s, m, row0, col0, mrow0, warp, g, t4, acc3, pre3);
         return;
     }
     // buffers: [buf][half] A tiles, then [buf][half] B tiles
@@ -288,6 +335,8 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
     const int nchunks = (hk + BK - 1) / BK;
     issue_A(0, 0);
     fetch_B(0);
+    double2 pre2[PF ? MT : 1][2][2];
+    if constexpr (PF) cgs_prefetch_add<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, pre2);
     store_B(0, 0);
     cp_async_wait_all();
     __syncthreads();
@@ -341,7 +390,7 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
 #pragma unroll
         for (int i = 0; i < MT; ++i) cmul3_finish(acc[hf][i], q2[hf][i]);
 #endif
-    cgs_epilogue<R2T, MODE, MT>(s, m, row0, col0, mrow0, warp, g, t4, acc);
+    cgs_epilogue<R2T, MODE, MT, PF>(s, m, row0, col0, mrow0, warp, g, t4, acc, pre2);
 }
 
 }  // namespace dev

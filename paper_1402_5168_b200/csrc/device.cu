@@ -34,7 +34,8 @@
 namespace rexp {
 namespace dev {
 
-void cgs_run(int mode, int R2, int MT, int WN, int nst, int K, dim3 grid, cudaStream_t s, const CgemmSymArgs& a);
+void cgs_run(int mode, int R2, int MT, int WN, int nst, bool pf, int K, dim3 grid, cudaStream_t s,
+             const CgemmSymArgs& a);
 void cgs_allow();
 
 __device__ __forceinline__ void cfma(double2& acc, const double2 a, const double2 b) {
@@ -1233,6 +1234,12 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         //   DOWN A_dn[o][r][(k, t) | nE q + (k, s')][(m, s, c)]
         //        = coef_s[t] (w.x | -w.y), w = -c2 d_mk Dinv_m(mode);   = (d_mk.x | -d_mk.y) if s = s'
         lg_KP = nF * q <= 44 ? 44 : 48;
+        {
+            const char* eu = std::getenv("REXP_LGU");
+            const char* ed = std::getenv("REXP_LGD");
+            lg_up_var = eu ? std::atoi(eu) : 1;   // 64 x 64 tiles (measured best on c3)
+            lg_dn_var = ed ? std::atoi(ed) : 0;
+        }
         lg_MT = nE * q + 2 * nE <= 48 ? 6 : 7;
         const size_t MR = 4 * static_cast<size_t>(nh), KP = lg_KP, MD = 8 * static_cast<size_t>(lg_MT);
         std::vector<double> Aup(2 * q * MR * KP, 0.0), Adn(2 * q * MD * MR, 0.0);
@@ -1349,7 +1356,14 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         nlanes = std::max(1, std::min(nlanes, std::min(nh, 4)));
     }
     {
-        size_t budget = static_cast<size_t>(16) << 30;   // 16 GiB of per-pole work buffers
+        // per-pole work buffers: most of the free device memory (one pole chunk per lane
+        // where it fits: every chunk re-reads and re-writes the leaf pole-sum partials),
+        // at least 16 GiB when that much is free
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const size_t margin = static_cast<size_t>(2) << 30;
+        size_t budget = fr > margin ? static_cast<size_t>(0.85 * static_cast<double>(fr - margin)) : 0;
+        budget = std::max(budget, std::min(static_cast<size_t>(16) << 30, static_cast<size_t>(0.85 * fr)));
         const char* env = std::getenv("REXP_CHUNK");
         chunk = env ? std::max(1, std::atoi(env)) : static_cast<int>(std::max<size_t>(1, budget / per_pole / nlanes));
         chunk = std::min(chunk, nh / nlanes);   // every lane's first chunk is full
@@ -1370,7 +1384,8 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
     if (fdm) {
         // K slices of the leaf DOWN GEMM: enough CTAs for ~4 per SM over the lanes
         // (REXP_GROUPS overrides); each slice owns a pole-sum partial slot
-        const long long ctas = 2LL * q * ((static_cast<long long>(nelem) * R2 + 127) / 128);
+        const int dbn = lg_dn_bn(lg_dn_var);
+        const long long ctas = 2LL * q * ((static_cast<long long>(nelem) * R2 + dbn - 1) / dbn);
         const char* env = std::getenv("REXP_GROUPS");
         ngroups = env ? std::atoi(env) : static_cast<int>((4LL * num_sms + ctas * nlanes - 1) / (ctas * nlanes));
         ngroups = std::max(1, std::min(ngroups, std::min(chunk, 32)));
@@ -1635,10 +1650,7 @@ void DeviceStore::configure_kernels() {
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cgs_allow();
-    cudaFuncSetAttribute(k_leaf_gemm_up<44>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_gemm_up<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_gemm_down<6, 128, LGD_NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_leaf_gemm_down<7, 128, LGD_NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    lg_allow();
     allow_all<2>();
     allow_all<4>();
     allow_all<8>();
@@ -1748,7 +1760,9 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
         a.nrowblk = (a.rows + bm - 1) / bm;
         const int ncb = (L.nodes * R2 + 8 * cfg.WN - 1) / (8 * cfg.WN);
         tbeg(s);
-        cgs_run(mode, R2, cfg.MT, cfg.WN, cfg.minb == 3 ? 3 : 2, a.K, dim3(a.nrowblk * ncb, pc), s, sa);
+        const int lo = cfg.minb & 15;
+        cgs_run(mode, R2, cfg.MT, cfg.WN, lo == 3 ? 3 : lo == 5 ? 12 : lo == 6 ? 11 : 2, (cfg.minb & 32) != 0, a.K,
+                dim3(a.nrowblk * ncb, pc), s, sa);
         tend(cls, s);
         return REXP_OK;
     }
@@ -1928,15 +1942,19 @@ int DeviceStore::tune_stages(bool measure) {
                         c.kind = 2; c.rb = rb; c.nb = nb;
                         cands.push_back(c);
                     }
-            for (int nst : {2, 3}) {
-                if (nst == 3 && kind == 0) continue;   // 3-stage ring: plain-gather modes (UP-Y, DOWN)
-                for (int mt : {2, 4})
-                    for (int wn : {2, 4, 8}) {
-                        StageCfg c;
-                        c.kind = 3; c.MT = mt; c.WN = wn; c.minb = nst == 3 ? 3 : 1;
-                        cands.push_back(c);
-                    }
-            }
+            // minb low bits: 1 register-staged B, 3 / 5 / 6 cp.async ring of 3 / 2 / 1 stage(s)
+            for (int nst : {1, 3, 5, 6})
+                for (int pf : {0, 32}) {
+                    if (nst != 1 && kind == 0) continue;   // rings: plain-gather modes (UP-Y, DOWN)
+                    if ((nst == 5 || nst == 6) && R2 != 128) continue;
+                    if (pf && (kind == 0 || R2 != 128)) continue;   // prefetched epilogue terms: UP-Y / DOWN, R2 = 128
+                    for (int mt : {2, 4})
+                        for (int wn : {2, 4, 8}) {
+                            StageCfg c;
+                            c.kind = 3; c.MT = mt; c.WN = wn; c.minb = nst | pf;
+                            cands.push_back(c);
+                        }
+                }
             float bt = time_cfg(kind, li, best);
             for (const StageCfg& c : cands) {
                 const float t = time_cfg(kind, li, c);
@@ -1993,7 +2011,8 @@ std::string DeviceStore::stage_report() const {
     auto one = [](const StageCfg& c) {
         if (c.kind == 3)
             return "symgemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
-                   (c.minb == 3 ? "s3" : "");
+                   ((c.minb & 15) == 3 ? "s3" : (c.minb & 15) == 5 ? "s2" : (c.minb & 15) == 6 ? "s1" : "") +
+                   (c.minb & 32 ? "pf" : "");
         return c.kind == 2 ? "sym" + std::to_string(c.rb) + (c.nb ? "n" + std::to_string(c.nb) : "")
                            : c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
@@ -2031,11 +2050,13 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
         lg.Ehat = d_Ehat + static_cast<size_t>(cur_lane) * ngroups * 2 * lg.ehat_ss;
         lg.Eedge = d_Eedge + static_cast<size_t>(cur_lane) * ngroups * lg.eedge_ss;
         lg.accumulate = m0 > lane_bufs[cur_lane].m0 ? 1 : 0;
-        const dim3 gu(static_cast<unsigned>((4 * pc + LGU_BM - 1) / LGU_BM),
-                      static_cast<unsigned>((lg.ncol + LGU_BN - 1) / LGU_BN), static_cast<unsigned>(2 * q));
+        int ubm, ubn;
+        lg_up_tile(lg_up_var, ubm, ubn);
+        const dim3 gu(static_cast<unsigned>((4 * pc + ubm - 1) / ubm),
+                      static_cast<unsigned>((lg.ncol + ubn - 1) / ubn), static_cast<unsigned>(2 * q));
         tbeg(s);
-        if (lg_KP == 44) k_leaf_gemm_up<44><<<gu, 32 * LGU_WM * LGU_WN, lg_up_smem<44>(), s>>>(lg);
-        else k_leaf_gemm_up<48><<<gu, 32 * LGU_WM * LGU_WN, lg_up_smem<48>(), s>>>(lg);
+        if (lg_KP == 44) lg_up_launch<44>(lg_up_var, gu, s, lg);
+        else lg_up_launch<48>(lg_up_var, gu, s, lg);
         tend(T_LEAF_UP, s);
     } else if (shared) {
         CgemmArgs a{};
@@ -2087,10 +2108,11 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
     }
     // ---- leaves down ----
     if (fdm) {
-        const dim3 gd(static_cast<unsigned>((lg.ncol + 127) / 128), static_cast<unsigned>(2 * q * ngroups));
+        const int dbn = lg_dn_bn(lg_dn_var);
+        const dim3 gd(static_cast<unsigned>((lg.ncol + dbn - 1) / dbn), static_cast<unsigned>(2 * q * ngroups));
         tbeg(s);
-        if (lg_MT == 6) k_leaf_gemm_down<6, 128, LGD_NST><<<gd, 128, lg_dn_smem<6, 128, LGD_NST>(), s>>>(lg);
-        else k_leaf_gemm_down<7, 128, LGD_NST><<<gd, 128, lg_dn_smem<7, 128, LGD_NST>(), s>>>(lg);
+        if (lg_MT == 6) lg_dn_launch<6>(lg_dn_var, gd, s, lg);
+        else lg_dn_launch<7>(lg_dn_var, gd, s, lg);
         tend(T_LEAF_DOWN, s);
     } else if (shared) {
         CgemmArgs a{};

@@ -66,20 +66,20 @@ struct LeafGemmArgs {
 // share the B tile (L2), every CTA of an (o, r) shares its A block.
 // Row order of A_up (chunk-local m): row 4 m + 2 s + c, c = 0 re, 1 im.
 // --------------------------------------------------------------------------
-constexpr int LGU_BM = 64, LGU_BN = 128, LGU_WM = 2, LGU_WN = 4;
 constexpr int LG_LDK = 52;    // row stride of A tiles (doubles), = 4 mod 16
 
-template <int KP>
+template <int KP, int BM, int BN>
 constexpr size_t lg_up_smem() {
-    return ((size_t)LGU_BM * LG_LDK + (size_t)KP * (LGU_BN + 4)) * sizeof(double);
+    return ((size_t)BM * LG_LDK + (size_t)KP * (BN + 4)) * sizeof(double);
 }
 
-template <int KP>
-__global__ void __launch_bounds__(32 * LGU_WM * LGU_WN) k_leaf_gemm_up(LeafGemmArgs a) {
-    constexpr int BM = LGU_BM, BN = LGU_BN, NT = 32 * LGU_WM * LGU_WN;
-    constexpr int TM = BM / LGU_WM, TN = BN / LGU_WN, MT = TM / 8, NTL = TN / 8;
+template <int KP, int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm_up(LeafGemmArgs a) {
+    constexpr int NT = 32 * WM * WN;
+    constexpr int TM = BM / WM, TN = BN / WN, MT = TM / 8, NTL = TN / 8;
     constexpr int LDB = BN + 4;
     static_assert(KP % 4 == 0 && KP + 4 <= LG_LDK, "K padding");
+    static_assert(MT % 2 == 0 || MT == 1, "m-tiles");
     extern __shared__ double lsm[];
     double* As = lsm;                   // [BM][LG_LDK]  A[row][k]
     double* Bs = lsm + BM * LG_LDK;     // [KP][LDB]     B[k][col]
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(32 * LGU_WM * LGU_WN) k_leaf_gemm_up(LeafGemmA
     const int mt0 = blockIdx.x * BM, col0 = blockIdx.y * BN;
     const int o = blockIdx.z / q, r = blockIdx.z % q;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int wm = wid / LGU_WN, wn = wid % LGU_WN;
+    const int wm = wid / WN, wn = wid % WN;
     const int g = lane >> 2, t4 = lane & 3;
     const double* A = a.Aup + (size_t)blockIdx.z * a.aup_os;
     // A rows [mt0, mt0 + BM): KP contiguous doubles each
@@ -283,6 +283,45 @@ __global__ void __launch_bounds__(BN) k_leaf_gemm_down(LeafGemmArgs a) {
                 }
             }
     }
+}
+
+// variant ids (REXP_LGU / REXP_LGD): UP 0 = 64x128 (2x4 warps), 1 = 64x64 (2x2),
+// 2 = 128x64 (4x2), 3 = 32x128 (1x4); DOWN 0 = BN 128 / 3 stages, 1 = 128 / 4,
+// 2 = 64 / 3, 3 = 64 / 4
+template <int KP>
+inline void lg_up_launch(int var, dim3 g3, cudaStream_t s, const LeafGemmArgs& a) {
+    switch (var) {
+        case 1: k_leaf_gemm_up<KP, 64, 64, 2, 2><<<g3, 128, lg_up_smem<KP, 64, 64>(), s>>>(a); break;
+        case 2: k_leaf_gemm_up<KP, 128, 64, 4, 2><<<g3, 256, lg_up_smem<KP, 128, 64>(), s>>>(a); break;
+        case 3: k_leaf_gemm_up<KP, 32, 128, 1, 4><<<g3, 128, lg_up_smem<KP, 32, 128>(), s>>>(a); break;
+        default: k_leaf_gemm_up<KP, 64, 128, 2, 4><<<g3, 256, lg_up_smem<KP, 64, 128>(), s>>>(a); break;
+    }
+}
+inline void lg_up_tile(int var, int& BM, int& BN) {
+    BM = var == 2 ? 128 : var == 3 ? 32 : 64;
+    BN = (var == 1 || var == 2) ? 64 : 128;
+}
+template <int MT>
+inline void lg_dn_launch(int var, dim3 g2, cudaStream_t s, const LeafGemmArgs& a) {
+    switch (var) {
+        case 1: k_leaf_gemm_down<MT, 128, 4><<<g2, 128, lg_dn_smem<MT, 128, 4>(), s>>>(a); break;
+        case 2: k_leaf_gemm_down<MT, 64, 3><<<g2, 64, lg_dn_smem<MT, 64, 3>(), s>>>(a); break;
+        case 3: k_leaf_gemm_down<MT, 64, 4><<<g2, 64, lg_dn_smem<MT, 64, 4>(), s>>>(a); break;
+        default: k_leaf_gemm_down<MT, 128, 3><<<g2, 128, lg_dn_smem<MT, 128, 3>(), s>>>(a); break;
+    }
+}
+inline int lg_dn_bn(int var) { return var >= 2 ? 64 : 128; }
+inline void lg_allow() {
+#define LG_ALLOW(...) cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+    LG_ALLOW(k_leaf_gemm_up<44, 64, 128, 2, 4>); LG_ALLOW(k_leaf_gemm_up<44, 64, 64, 2, 2>);
+    LG_ALLOW(k_leaf_gemm_up<44, 128, 64, 4, 2>); LG_ALLOW(k_leaf_gemm_up<44, 32, 128, 1, 4>);
+    LG_ALLOW(k_leaf_gemm_up<48, 64, 128, 2, 4>); LG_ALLOW(k_leaf_gemm_up<48, 64, 64, 2, 2>);
+    LG_ALLOW(k_leaf_gemm_up<48, 128, 64, 4, 2>); LG_ALLOW(k_leaf_gemm_up<48, 32, 128, 1, 4>);
+    LG_ALLOW(k_leaf_gemm_down<6, 128, 3>); LG_ALLOW(k_leaf_gemm_down<6, 128, 4>);
+    LG_ALLOW(k_leaf_gemm_down<6, 64, 3>); LG_ALLOW(k_leaf_gemm_down<6, 64, 4>);
+    LG_ALLOW(k_leaf_gemm_down<7, 128, 3>); LG_ALLOW(k_leaf_gemm_down<7, 128, 4>);
+    LG_ALLOW(k_leaf_gemm_down<7, 64, 3>); LG_ALLOW(k_leaf_gemm_down<7, 64, 4>);
+#undef LG_ALLOW
 }
 
 }  // namespace dev

@@ -114,6 +114,7 @@ class DeviceStore {
     int* d_leaf_own = nullptr;                  // [nelem][4q] edge-node ownership for the pole sums
     double *d_Aup = nullptr, *d_Adn = nullptr;  // leaf GEMM coefficients (leaf_gemm.cuh), [2q][..]
     int lg_KP = 44, lg_MT = 6;                  // their K padding (UP) / row tiles (DOWN)
+    int lg_up_var = 0, lg_dn_var = 0;           // tile variants (leaf_gemm.cuh)
     int ngroups = 1;                            // K slices of the leaf DOWN GEMM = pole-sum partial slots per lane
     int chunk = 1;             // half poles per work-buffer chunk
     int num_sms = 148;
