@@ -158,9 +158,14 @@ __device__ __forceinline__ void cg_store(const CgemmArgs& a, int m, int row, int
     }
 }
 
+// NST: 2 = B through registers (double-buffered), 3 = cp.async ring of 3 stages,
+// 11 = cp.async, one stage (short-K levels: small footprint, more CTAs per SM)
+template <int NST>
+__host__ __device__ constexpr int cg_ring() { return NST >= 10 ? NST - 10 : NST; }
 template <int MT, int WN, int BK, int NTW = 1, int WM = 1, int NST = 2>
 __host__ __device__ constexpr size_t cgemm_smem_bytes() {
-    return (size_t)NST * BK * ((8 * MT * WM + 2) + (8 * WN * NTW + 2)) * sizeof(double2);
+    return (size_t)(cg_ring<NST>() < 2 ? 2 : cg_ring<NST>()) * BK * ((8 * MT * WM + 2) + (8 * WN * NTW + 2)) *
+           sizeof(double2);
 }
 // UP-Y (compile-time R2): the additive child term of the tile is staged too
 template <int MT, int WN, int BK, int NTW = 1, int WM = 1, int NST = 2, int MODE = 0>
@@ -358,8 +363,9 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
         }
     };
     if constexpr (NST >= 3 && cg_plain_b<MODE>()) {
+        constexpr int RS = cg_ring<NST>();
         auto AsN = [&](int buf) { return sm + buf * BK * LDA; };
-        auto BsN = [&](int buf) { return sm + NST * BK * LDA + buf * BK * LDB; };
+        auto BsN = [&](int buf) { return sm + (RS < 2 ? 2 : RS) * BK * LDA + buf * BK * LDB; };
         auto issue = [&](int buf, int k0) {
             double2* ab = AsN(buf);
             for (int e = tid; e < BK * BM; e += NT) {
@@ -378,17 +384,25 @@ __global__ void __launch_bounds__(32 * WN * WM, MINB) k_cgemm(CgemmArgs a) {
             cp_async_commit();
         };
 #pragma unroll
-        for (int st = 0; st < NST - 1; ++st) {
+        for (int st = 0; st < RS - 1; ++st) {
             if (st < nchunks) issue(st, st * BK);
             else cp_async_commit();
         }
         for (int ch = 0; ch < nchunks; ++ch) {
-            cp_async_wait_group<NST - 2>();   // chunk ch has landed (this thread's copies)
-            __syncthreads();                  // everyone's copies; the buffer refilled below is free
-            const int nx = ch + NST - 1;
-            if (nx < nchunks) issue(nx % NST, nx * BK);
-            else cp_async_commit();
-            compute(AsN(ch % NST), BsN(ch % NST));
+            if constexpr (RS == 1) {
+                if (ch > 0) __syncthreads();  // everyone is done with the single stage
+                issue(0, ch * BK);
+                cp_async_wait_all();
+                __syncthreads();
+                compute(AsN(0), BsN(0));
+            } else {
+                cp_async_wait_group<(RS >= 2 ? RS - 2 : 0)>();   // chunk ch has landed (this thread's copies)
+                __syncthreads();                  // everyone's copies; the buffer refilled below is free
+                const int nx = ch + RS - 1;
+                if (nx < nchunks) issue(nx % RS, nx * BK);
+                else cp_async_commit();
+                compute(AsN(ch % RS), BsN(ch % RS));
+            }
         }
     } else {
         issue_A(0, 0);

@@ -45,8 +45,26 @@ void cg_tiles_s3(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) 
         cg_tiles_b<BK, R2T, MODE, 1>(MT, WN, grid, s, a);
     }
 }
+// single-stage cp.async (plain-gather B modes, R2 = 128): short-K levels
+template <int BK, int R2T, int MODE>
+void cg_tiles_s1(int MT, int WN, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
+    if constexpr ((MODE == CG_UPY || MODE == CG_DOWN) && R2T == 128) {
+        if (MT == 2) {
+            if (WN == 2) cg_launch<2, 2, BK, R2T, MODE, 4, 1, 11>(grid, s, a);
+            else if (WN == 4) cg_launch<2, 4, BK, R2T, MODE, 2, 1, 11>(grid, s, a);
+            else cg_launch<2, 8, BK, R2T, MODE, 1, 1, 11>(grid, s, a);
+        } else {
+            if (WN == 2) cg_launch<4, 2, BK, R2T, MODE, 4, 1, 11>(grid, s, a);
+            else if (WN == 4) cg_launch<4, 4, BK, R2T, MODE, 2, 1, 11>(grid, s, a);
+            else cg_launch<4, 8, BK, R2T, MODE, 1, 1, 11>(grid, s, a);
+        }
+    } else {
+        cg_tiles_s3<BK, R2T, MODE>(MT, WN, grid, s, a);
+    }
+}
 // MINB = 4: register budget for 4 resident 256-thread CTAs per SM (<= 64 registers);
-// MINB = 3 selects the 3-stage cp.async pipeline instead (StageCfg::minb)
+// MINB = 3 selects the 3-stage cp.async pipeline instead (StageCfg::minb), 6 the
+// single-stage one
 template <int BK, int R2T, int MODE>
 void cg_tiles(int MT, int WN, int MINB, dim3 grid, cudaStream_t s, const CgemmArgs& a) {
     if (MODE == CG_LEAF_UP || MODE == CG_LEAF_DOWN) {
@@ -54,7 +72,8 @@ void cg_tiles(int MT, int WN, int MINB, dim3 grid, cudaStream_t s, const CgemmAr
         else cg_launch<5, 8, BK, R2T, MODE>(grid, s, a);
         return;
     }
-    if (MINB >= 4) cg_tiles_b<BK, R2T, MODE, 4>(MT, WN, grid, s, a);
+    if (MINB == 6) cg_tiles_s1<BK, R2T, MODE>(MT, WN, grid, s, a);
+    else if (MINB >= 4) cg_tiles_b<BK, R2T, MODE, 4>(MT, WN, grid, s, a);
     else if (MINB == 3) cg_tiles_s3<BK, R2T, MODE>(MT, WN, grid, s, a);
     else cg_tiles_b<BK, R2T, MODE, 1>(MT, WN, grid, s, a);
 }
@@ -77,6 +96,11 @@ void cg_allow_tiles() {
         cg_allow1<2, 2, BK, R2T, MODE, 4, 1, 3>(); cg_allow1<2, 4, BK, R2T, MODE, 2, 1, 3>();
         cg_allow1<2, 8, BK, R2T, MODE, 1, 1, 3>(); cg_allow1<4, 2, BK, R2T, MODE, 4, 1, 3>();
         cg_allow1<4, 4, BK, R2T, MODE, 2, 1, 3>(); cg_allow1<4, 8, BK, R2T, MODE, 1, 1, 3>();
+    }
+    if constexpr ((MODE == CG_UPY || MODE == CG_DOWN) && R2T == 128) {
+        cg_allow1<2, 2, BK, R2T, MODE, 4, 1, 11>(); cg_allow1<2, 4, BK, R2T, MODE, 2, 1, 11>();
+        cg_allow1<2, 8, BK, R2T, MODE, 1, 1, 11>(); cg_allow1<4, 2, BK, R2T, MODE, 4, 1, 11>();
+        cg_allow1<4, 4, BK, R2T, MODE, 2, 1, 11>(); cg_allow1<4, 8, BK, R2T, MODE, 1, 1, 11>();
     }
 }
 

@@ -1969,8 +1969,9 @@ int DeviceStore::tune_stages(bool measure) {
         for (int bk16 : {0, 16}) {
             if (!shared) break;
             if (bk16 && Kst % 28 != 0) continue;
-            for (int minb : {1, 4, 3}) {
+            for (int minb : {1, 4, 3, 6}) {
                 if (minb == 3 && kind != 1 && kind != 2) continue;
+                if (minb == 6 && ((kind != 1 && kind != 2) || R2 != 128)) continue;   // single-stage cp.async
                 for (int mt : {2, 4})
                     for (int wn : {2, 4, 8}) {
                         StageCfg c;
@@ -2016,7 +2017,8 @@ std::string DeviceStore::stage_report() const {
         return c.kind == 2 ? "sym" + std::to_string(c.rb) + (c.nb ? "n" + std::to_string(c.nb) : "")
                            : c.kind == 1 ? "gemv" + std::to_string(c.rb)
                            : "gemm" + std::to_string(8 * c.MT * cg_wm(c.WN)) + "x" + std::to_string(8 * c.WN) +
-                                 ((c.minb & 15) == 4 ? "r" : (c.minb & 15) == 3 ? "s3" : "") + (c.minb & 16 ? "k16" : "");
+                                 ((c.minb & 15) == 4 ? "r" : (c.minb & 15) == 3 ? "s3" : (c.minb & 15) == 6 ? "s1" : "") +
+                                 (c.minb & 16 ? "k16" : "");
     };
     std::string s = tuned ? "tuned:" : "default:";
     for (size_t li = 0; li < levels.size(); ++li)
