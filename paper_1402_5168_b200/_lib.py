@@ -3,7 +3,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librexp.so")
+# REXP_LIB: an alternative in-tree build of the same library (e.g. one compiled
+# with -DREXP_CMUL3=0 for accuracy experiments); the default is librexp.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("REXP_LIB", "librexp.so"))
 
 
 class RexpProblem(ctypes.Structure):

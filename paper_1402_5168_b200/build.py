@@ -24,9 +24,15 @@ def _run(cmd):
     subprocess.check_call(cmd)
 
 
-def build(force=False, verbose_ptxas=False):
-    """Compile every translation unit (in parallel) and link librexp.so."""
+def build(force=False, verbose_ptxas=False, variant=None):
+    """Compile every translation unit (in parallel) and link librexp.so.
+    variant="cmul4": an experiment build (librexp_cmul4.so, four real DMMAs per
+    complex k-step instead of the three-multiply form) loaded with REXP_LIB."""
     import concurrent.futures as cf
+    BUILD, LIB = globals()["BUILD"], globals()["LIB"]
+    extra = []
+    if variant == "cmul4":
+        BUILD, LIB, extra = BUILD + "_cmul4", os.path.join(HERE, "librexp_cmul4.so"), ["-DREXP_CMUL3=0"]
     os.makedirs(BUILD, exist_ok=True)
     srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     srcs.append(os.path.join(os.path.dirname(HERE), "include", "rexp.h"))
@@ -38,14 +44,14 @@ def build(force=False, verbose_ptxas=False):
     jobs = []
     for f in CU:
         o = os.path.join(BUILD, f + ".o")
-        cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c",
+        cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra, "-c",
                os.path.join(CSRC, f), "-o", o]
         if verbose_ptxas:
             cmd.insert(1, "-Xptxas=-v")
         jobs.append((cmd, o))
     for mode in range(6):   # k_cgemm tile instantiations, one object per mode
         o = os.path.join(BUILD, f"cgemm_mode{mode}.o")
-        jobs.append(([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-DCG_MODE={mode}",
+        jobs.append(([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra, f"-DCG_MODE={mode}",
                       "-c", os.path.join(CSRC, "cgemm_mode.cu"), "-o", o], o))
     for f in CPP:
         o = os.path.join(BUILD, f + ".o")
@@ -61,4 +67,5 @@ def build(force=False, verbose_ptxas=False):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv,
+          variant="cmul4" if "--cmul4" in sys.argv else None)
