@@ -14,7 +14,7 @@ LIB = os.path.join(HERE, "librexp.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
-CU = ["device.cu", "cgemm_sym.cu"]
+CU = ["device.cu", "cgemm_sym.cu", "fused_tree.cu"]
 CPP = ["rational.cpp", "mesh.cpp", "setup_host.cpp", "eig.cpp", "api.cpp"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1327,6 +1327,14 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         if ((rc = put(&D.ext, L.ext))) return rc;
         if ((rc = put(&D.gext, L.gext))) return rc;
         if ((rc = put(&D.g3, L.g3))) return rc;
+        {
+            // node-independent forms of the gathers (node 0's rows) for the fused sweeps
+            std::vector<int32_t> ec(L.ext_is_b.begin(), L.ext_is_b.begin() + L.next);
+            std::vector<int32_t> ep(L.ext_pos.begin(), L.ext_pos.begin() + L.next);
+            if ((rc = put(&D.ia3p, L.ia3_pos)) || (rc = put(&D.ib3p, L.ib3_pos)) || (rc = put(&D.extc, ec)) ||
+                (rc = put(&D.extp, ep)))
+                return rc;
+        }
     }
     ns = T.ns;
     // shared store: n Fourier blocks of the block-circulant seam operator
@@ -1421,6 +1429,7 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         use_graph = !(env && std::string(env) == "0");
     }
     configure_kernels();
+    if ((rc = plan_fused())) return rc;
     return tune_stages(false);
 }
 
@@ -1650,6 +1659,7 @@ void DeviceStore::configure_kernels() {
     cudaFuncSetAttribute(k_leaf_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cgs_allow();
+    ft_allow();
     lg_allow();
     allow_all<2>();
     allow_all<4>();
@@ -1660,7 +1670,10 @@ int DeviceStore::launches_per_step() const {
     int nchunks = 0;
     for (const auto& B : lane_bufs) nchunks += (B.m1 - B.m0 + chunk - 1) / chunk;
     const int per_chunk = (shared && !fdm ? 5 : 4) + 3 * static_cast<int>(levels.size());
-    return fdm ? 3 + nchunks * (3 + 3 * static_cast<int>(levels.size())) : 2 + nchunks * per_chunk;
+    int fused_saved = 0;   // a fused UP group replaces 2 launches per level, a DOWN group 1 per level
+    for (const auto& g : ft_up) fused_saved += 2 * g.nlev - 1;
+    for (const auto& g : ft_down) fused_saved += g.nlev - 1;
+    return fdm ? 3 + nchunks * (3 + 3 * static_cast<int>(levels.size()) - fused_saved) : 2 + nchunks * per_chunk;
 }
 
 int DeviceStore::check(const char* what) {
@@ -1679,7 +1692,7 @@ int DeviceStore::check(const char* what) {
 // with either the DMMA GEMM (cfg.kind 0, tile cfg.MT x cfg.WN) or the GEMV kernel.
 int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, int pc, cudaStream_t s) {
     if (kind == 3) {
-        const double2* hr = d_h[levels.size() % 2];
+        const double2* hr = d_h[h_sel >= 0 ? h_sel : static_cast<int>(levels.size() % 2)];
         const double2* Xr = d_Xroot + static_cast<size_t>(m0) * pp_Xroot;
         if (shared) {
             RootFArgs a{};
@@ -1714,8 +1727,9 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
         return REXP_OK;
     }
     Level& L = levels[li];
-    const double2* hc = d_h[li % 2];
-    double2* hp = d_h[(li + 1) % 2];
+    const int hb = h_sel >= 0 ? h_sel : static_cast<int>(li % 2);
+    const double2* hc = d_h[hb];
+    double2* hp = d_h[hb ^ 1];
     const int cls = kind == 2 ? T_MERGE_DOWN : T_MERGE_UP;
     if (kind == 0 && L.xdiag) {
         UpxDiagArgs u{};
@@ -1861,6 +1875,82 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
     return REXP_OK;
 }
 
+// Fused subtree sweeps (fused_tree.cu), spectral shared store only.  REXP_FUSE_UP /
+// REXP_FUSE_DOWN: group sizes from the lowest level up, e.g. "2,2" = levels (1,2)
+// and (3,4) each in one kernel; "0" = none.
+int DeviceStore::plan_fused() {
+    ft_up.clear();
+    ft_down.clear();
+    if (!(shared && fdm)) return REXP_OK;
+    auto parse = [](const char* env, const char* dflt) {
+        std::vector<int> v;
+        std::string t = env ? env : dflt;
+        size_t p = 0;
+        while (p < t.size()) {
+            size_t e = t.find(',', p);
+            if (e == std::string::npos) e = t.size();
+            v.push_back(std::atoi(t.substr(p, e - p).c_str()));
+            p = e + 1;
+        }
+        return v;
+    };
+    auto build = [&](const std::vector<int>& sizes, bool down, std::vector<FtGroup>& out) {
+        int l0 = 0;
+        for (int nlev : sizes) {
+            if (nlev < 1 || l0 + nlev > static_cast<int>(levels.size())) break;
+            if (nlev == 1) { ++l0; continue; }
+            FtGroup g;
+            g.l0 = l0; g.nlev = nlev;
+            FtArgs& a = g.args;
+            a = FtArgs{};
+            a.nlev = nlev; a.R2 = R2; a.hps = hstride; a.NE = NE;
+            for (int l = 0; l < nlev && l < FT_MAXLEV; ++l) {
+                const Level& D = levels[l0 + l];
+                FtLevel& F = a.lv[l];
+                F.X = D.X; F.Y = D.Y; F.S = D.S; F.ppX = D.ppX; F.ppY = D.ppY; F.ppS = D.ppS;
+                F.n3 = D.n3; F.next = D.next; F.nchild = D.nchild; F.nbx = D.nbx; F.xdir = D.dir == 0 ? 1 : 0;
+                F.sym = D.sym ? 1 : 0; F.xdiag = D.xdiag ? 1 : 0; F.nodes = D.nodes;
+                F.ia3p = D.ia3p; F.ib3p = D.ib3p; F.extc = D.extc; F.extp = D.extp;
+                F.siA = D.siA; F.siB = D.siB; F.seA = D.seA; F.seB = D.seB; F.sis = D.sis; F.ses = D.ses;
+                F.gext = D.gext; F.g3 = D.g3;
+            }
+            if (ft_plan(a, down)) out.push_back(g);
+            l0 += nlev;
+        }
+    };
+    build(parse(std::getenv("REXP_FUSE_UP"), "2,2"), false, ft_up);
+    build(parse(std::getenv("REXP_FUSE_DOWN"), "2,2"), true, ft_down);
+    return REXP_OK;
+}
+
+const DeviceStore::FtGroup* DeviceStore::ft_group(const std::vector<FtGroup>& v, int l0) const {
+    for (const FtGroup& g : v)
+        if (g.l0 == l0) return &g;
+    return nullptr;
+}
+
+int DeviceStore::launch_fused(const FtGroup& g, bool down, int m0, int pc, cudaStream_t s) {
+    FtArgs a = g.args;
+    for (int l = 0; l < g.nlev; ++l) {
+        const Level& D = levels[g.l0 + l];
+        FtLevel& F = a.lv[l];
+        F.X = D.X + static_cast<size_t>(m0) * D.ppX;
+        F.Y = D.Y + static_cast<size_t>(m0) * D.ppY;
+        F.S = D.S + static_cast<size_t>(m0) * D.ppS;
+        F.w3 = D.w3;
+    }
+    const int hb = h_sel >= 0 ? h_sel : g.l0 % 2;
+    a.hin = d_h[hb];
+    a.hout = d_h[hb ^ 1];
+    a.edge = d_edge;
+    const int top_nodes = levels[g.l0 + g.nlev - 1].nodes;
+    tbeg(s);
+    if (down) ft_launch_down(a, top_nodes, pc, s);
+    else ft_launch_up(a, top_nodes, pc, s);
+    tend(down ? T_MERGE_DOWN : T_MERGE_UP, s);
+    return REXP_OK;
+}
+
 // default stage choices, then (REXP_AUTOTUNE != 0) time every candidate on the
 // real buffers and keep the fastest: DMMA GEMM tiles MT in {2, 4} x WN in
 // {2, 4, 8} (shared store) and the GEMV kernel (nrhs <= 4)
@@ -1932,7 +2022,7 @@ int DeviceStore::tune_stages(bool measure) {
         }
         return total;
     };
-    auto tune = [&](int kind, size_t li, StageCfg& best) {
+    auto tune = [&](int kind, size_t li, StageCfg& best) -> float {
         std::vector<StageCfg> cands;
         if (kind != 3 && levels[li].sym) {
             if (gemv_ok)
@@ -1960,7 +2050,7 @@ int DeviceStore::tune_stages(bool measure) {
                 const float t = time_cfg(kind, li, c);
                 if (t < bt) { bt = t; best = c; }
             }
-            return;
+            return bt;
         }
         // minb: 1 = default, 4 = register-capped, 3 = 3-stage cp.async ring (UP-Y / DOWN);
         // + 16: BK = 16 where K is a multiple of 28 (smaller footprint)
@@ -1992,11 +2082,48 @@ int DeviceStore::tune_stages(bool measure) {
             const float t = time_cfg(kind, li, c);
             if (t < bt) { bt = t; best = c; }
         }
+        return bt;
     };
+    std::vector<float> tu(nl, 0.f), td(nl, 0.f);   // best single-level times (3 cold launches)
     for (size_t li = 0; li < nl; ++li) {
-        if (!levels[li].xdiag) tune(0, li, t_upx[li]);
-        tune(1, li, t_upy[li]);
-        tune(2, li, t_down[li]);
+        tu[li] = levels[li].xdiag ? time_cfg(0, li, t_upx[li]) : tune(0, li, t_upx[li]);
+        tu[li] += tune(1, li, t_upy[li]);
+        td[li] = tune(2, li, t_down[li]);
+    }
+    {
+        // a fused group stays only if it beats its levels' tuned single launches
+        auto time_group = [&](const FtGroup& g, bool down) -> float {
+            if (launch_fused(g, down, 0, pc, s) != REXP_OK) return 1e30f;
+            float total = 0.f;
+            for (int r = 0; r < 3; ++r) {
+                if (flush) cudaMemsetAsync(flush, r, flush_bytes, s);
+                cudaEventRecord(e0, s);
+                launch_fused(g, down, 0, pc, s);
+                cudaEventRecord(e1, s);
+                cudaEventSynchronize(e1);
+                if (cudaGetLastError() != cudaSuccess) return 1e30f;
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                total += ms;
+            }
+            return total;
+        };
+        const char* keep = std::getenv("REXP_FUSE_FORCE");
+        auto prune = [&](std::vector<FtGroup>& v, bool down, const std::vector<float>& single) {
+            std::vector<FtGroup> out;
+            for (const FtGroup& g : v) {
+                float ts = 0.f;
+                for (int l = 0; l < g.nlev; ++l) ts += single[g.l0 + l];
+                const float tf = time_group(g, down);
+                ft_times += (down ? " down" : " up") + std::to_string(g.l0 + 1) + "-" + std::to_string(g.l0 + g.nlev) +
+                            ":" + std::to_string(tf / 3) + "/" + std::to_string(ts / 3) + "ms";
+                if (tf < ts || keep) out.push_back(g);
+            }
+            v.swap(out);
+        };
+        ft_times.clear();
+        prune(ft_up, false, tu);
+        prune(ft_down, true, td);
     }
     if (!shared) tune(3, 0, t_root);
     timing = saved_timing;
@@ -2025,6 +2152,9 @@ std::string DeviceStore::stage_report() const {
         s += " L" + std::to_string(li + 1) + "[" + (levels[li].xdiag ? std::string("diag") : one(t_upx[li])) + "," +
              one(t_upy[li]) + "," + one(t_down[li]) + "]";
     s += shared ? std::string(" root[fourier]") : " root[" + one(t_root) + "]";
+    for (const auto& g : ft_up) s += " fused_up[L" + std::to_string(g.l0 + 1) + "-L" + std::to_string(g.l0 + g.nlev) + "]";
+    for (const auto& g : ft_down) s += " fused_down[L" + std::to_string(g.l0 + g.nlev) + "-L" + std::to_string(g.l0 + 1) + "]";
+    if (!ft_times.empty()) s += " fused_vs_single:" + ft_times;
     return s;
 }
 
@@ -2092,21 +2222,39 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
         }
         tend(T_LEAF_UP, s);
     }
-    // ---- merges up ----
-    for (size_t li = 0; li < levels.size(); ++li) {
+    // ---- merges up (h ping-pongs between the two buffers once per launch unit) ----
+    h_sel = 0;
+    for (size_t li = 0; li < levels.size();) {
         int rc;
-        if ((rc = launch_stage(0, li, t_upx[li], m0, pc, s))) return rc;
-        if ((rc = launch_stage(1, li, t_upy[li], m0, pc, s))) return rc;
+        if (const FtGroup* g = ft_group(ft_up, static_cast<int>(li))) {
+            if ((rc = launch_fused(*g, false, m0, pc, s))) return rc;
+            li += static_cast<size_t>(g->nlev);
+        } else {
+            if ((rc = launch_stage(0, li, t_upx[li], m0, pc, s))) return rc;
+            if ((rc = launch_stage(1, li, t_upy[li], m0, pc, s))) return rc;
+            ++li;
+        }
+        h_sel ^= 1;
     }
     // ---- periodic closure ----
     {
         int rc;
         if ((rc = launch_stage(3, 0, t_root, m0, pc, s))) return rc;
     }
+    h_sel = -1;
     // ---- merges down ----
-    for (int li = static_cast<int>(levels.size()) - 1; li >= 0; --li) {
+    for (int li = static_cast<int>(levels.size()) - 1; li >= 0;) {
         int rc;
-        if ((rc = launch_stage(2, static_cast<size_t>(li), t_down[li], m0, pc, s))) return rc;
+        const FtGroup* g = nullptr;
+        for (const FtGroup& c : ft_down)
+            if (c.l0 + c.nlev - 1 == li) g = &c;
+        if (g) {
+            if ((rc = launch_fused(*g, true, m0, pc, s))) return rc;
+            li -= g->nlev;
+        } else {
+            if ((rc = launch_stage(2, static_cast<size_t>(li), t_down[li], m0, pc, s))) return rc;
+            --li;
+        }
     }
     // ---- leaves down ----
     if (fdm) {

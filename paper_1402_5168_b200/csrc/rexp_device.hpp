@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "fused_tree.hpp"
 #include "rexp_internal.hpp"
 
 namespace rexp {
@@ -29,6 +30,7 @@ struct Level {
     std::vector<double> h_is, h_es;
     double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
     int *ia3 = nullptr, *ib3 = nullptr, *ext = nullptr, *gext = nullptr, *g3 = nullptr;
+    int *ia3p = nullptr, *ib3p = nullptr, *extc = nullptr, *extp = nullptr;   // node-independent forms (fused sweeps)
     double2* w3 = nullptr;                              // [chunk][nodes][n3][R2]
     size_t ppX = 0, ppY = 0, ppS = 0;                   // per-pole operator sizes (complex)
 };
@@ -127,6 +129,14 @@ class DeviceStore {
     bool tuned = false;
     private:
     std::vector<StageCfg> t_upx, t_upy, t_down;
+    // fused subtree sweeps (fused_tree.cu): groups of consecutive levels run by one kernel
+    struct FtGroup { int l0 = 0, nlev = 0; FtArgs args; };
+    std::vector<FtGroup> ft_up, ft_down;   // by lowest level, ascending
+    std::string ft_times;                  // autotuner: fused vs single-level times
+    int h_sel = -1;                        // h buffer holding the current children (-1: by level parity)
+    int plan_fused();
+    const FtGroup* ft_group(const std::vector<FtGroup>& v, int l0) const;
+    int launch_fused(const FtGroup& g, bool down, int m0, int pc, cudaStream_t s);
     StageCfg t_root;
     SpecArgs spec_args(int m0, int pc) const;
     int pole_sum_chunk(int m0, int pc, bool accumulate, double* d_E_out, cudaStream_t s);

@@ -175,6 +175,32 @@ def test_config0_symmetric_pair_gemm_many_rhs(c0, nrhs, stages, monkeypatch):
     h.close()
 
 
+@pytest.mark.parametrize("nrhs,up,down", [(1, "2", "2"), (2, "2", "0"), (4, "0", "2"), (8, "2", "2"), (64, "2", "2"),
+                                          (8, "3", "3"), (4, "3", "3")])
+def test_config0_fused_subtree_sweeps(c0, nrhs, up, down, monkeypatch):
+    """The fused multi-level merge kernels (fused_tree.cu: boundary data of a
+    subtree resident in shared memory, operators streamed by bulk copies on
+    mbarriers) forced on (REXP_FUSE_FORCE keeps them even where the autotuner
+    would prefer the single-level launches): levels (1, 2) upward and (2, 1)
+    downward, separately and together, and all three levels of config 0's tree in
+    one kernel; column layouts RC = 2, 4, 8 (R2 = 2, 4, 8 and wider)."""
+    cfg, m, op, u0 = c0
+    Lam = cfg["Lambda_tau"] / cfg["tau"]
+    monkeypatch.setenv("REXP_FUSE_UP", up)
+    monkeypatch.setenv("REXP_FUSE_DOWN", down)
+    monkeypatch.setenv("REXP_FUSE_FORCE", "1")
+    U = np.stack([rsw_initial_state(m.x, m.y, cfg["seed"] + 10 * k) for k in range(nrhs)])
+    h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], nrhs=nrhs)
+    rep = h.stage_report
+    assert ("fused_up" in rep) == (up != "0") and ("fused_down" in rep) == (down != "0"), rep
+    got = _gpu_apply(h, U, 2)
+    ks = range(0, nrhs, max(1, nrhs // 4))
+    errs = [rel_l2(got[k], op.evolve(U[k], 2)) for k in ks]
+    print(f"fused sweeps nrhs {nrhs} up {up} down {down}: max rel L2 {max(errs):.3e}")
+    assert max(errs) <= TOL
+    h.close()
+
+
 def test_config0_long_run_accumulation(c0):
     """60 steps (graph replay, pole lanes): the error against the oracle must not
     grow beyond the per-step rounding (no drift from the spectral / pair /
