@@ -1429,7 +1429,7 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         use_graph = !(env && std::string(env) == "0");
     }
     configure_kernels();
-    if ((rc = plan_fused())) return rc;
+    if ((rc = plan_fused(T))) return rc;
     return tune_stages(false);
 }
 
@@ -1480,6 +1480,7 @@ int DeviceStore::sym_pairs(const Tree& T, const MergeLevel& L, Level& D) {
 
 // copy the host factorization of local half poles [m0, m0 + count) into the store
 int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
+    ft_packed = false;   // the fused kernels' operator images are rebuilt from the new store
     auto up = [&](const std::vector<cd>& v, double2* dst, size_t per_pole) -> int {
         if (per_pole == 0 || v.empty()) return REXP_OK;
         std::vector<double2> tmp(v.size());
@@ -1878,9 +1879,10 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
 // Fused subtree sweeps (fused_tree.cu), spectral shared store only.  REXP_FUSE_UP /
 // REXP_FUSE_DOWN: group sizes from the lowest level up, e.g. "2,2" = levels (1,2)
 // and (3,4) each in one kernel; "0" = none.
-int DeviceStore::plan_fused() {
+int DeviceStore::plan_fused(const Tree& T) {
     ft_up.clear();
     ft_down.clear();
+    ft_packed = false;
     if (!(shared && fdm)) return REXP_OK;
     auto parse = [](const char* env, const char* dflt) {
         std::vector<int> v;
@@ -1894,33 +1896,69 @@ int DeviceStore::plan_fused() {
         }
         return v;
     };
+    int rc = REXP_OK;
     auto build = [&](const std::vector<int>& sizes, bool down, std::vector<FtGroup>& out) {
         int l0 = 0;
         for (int nlev : sizes) {
             if (nlev < 1 || l0 + nlev > static_cast<int>(levels.size())) break;
-            if (nlev == 1) { ++l0; continue; }
+            if (nlev == 1 || nlev > FT_MAXLEV) { l0 += nlev; continue; }
             FtGroup g;
             g.l0 = l0; g.nlev = nlev;
             FtArgs& a = g.args;
             a = FtArgs{};
             a.nlev = nlev; a.R2 = R2; a.hps = hstride; a.NE = NE;
-            for (int l = 0; l < nlev && l < FT_MAXLEV; ++l) {
+            FtHostLevel hl[FT_MAXLEV];
+            for (int l = 0; l < nlev; ++l) {
                 const Level& D = levels[l0 + l];
+                const MergeLevel& M = T.levels[l0 + l];
                 FtLevel& F = a.lv[l];
                 F.X = D.X; F.Y = D.Y; F.S = D.S; F.ppX = D.ppX; F.ppY = D.ppY; F.ppS = D.ppS;
                 F.n3 = D.n3; F.next = D.next; F.nchild = D.nchild; F.nbx = D.nbx; F.xdir = D.dir == 0 ? 1 : 0;
                 F.sym = D.sym ? 1 : 0; F.xdiag = D.xdiag ? 1 : 0; F.nodes = D.nodes;
-                F.ia3p = D.ia3p; F.ib3p = D.ib3p; F.extc = D.extc; F.extp = D.extp;
-                F.siA = D.siA; F.siB = D.siB; F.seA = D.seA; F.seB = D.seB; F.sis = D.sis; F.ses = D.ses;
                 F.gext = D.gext; F.g3 = D.g3;
+                hl[l].ia3p.assign(M.ia3_pos.begin(), M.ia3_pos.end());
+                hl[l].ib3p.assign(M.ib3_pos.begin(), M.ib3_pos.end());
+                hl[l].extc.assign(M.ext_is_b.begin(), M.ext_is_b.begin() + M.next);
+                hl[l].extp.assign(M.ext_pos.begin(), M.ext_pos.begin() + M.next);
+                hl[l].iA = D.h_iA; hl[l].iB = D.h_iB; hl[l].eA = D.h_eA; hl[l].eB = D.h_eB;
+                hl[l].is = D.h_is; hl[l].es = D.h_es;
             }
-            if (ft_plan(a, down)) out.push_back(g);
+            std::vector<int> itab;
+            std::vector<double> dtab;
+            if (ft_plan(a, hl, down, itab, dtab)) {
+                int* di = nullptr;
+                double* dd = nullptr;
+                if ((rc = put(&di, itab)) || (rc = put(&dd, dtab))) return;
+                a.itab = di; a.dtab = dd;
+                // chunked, padded operator images of every half pole (ft_pack after the upload)
+                if ((rc = alloc(&g.img, static_cast<size_t>(nh) * a.img_ps))) return;
+                store_bytes += static_cast<int64_t>(nh) * a.img_ps * 16;
+                out.push_back(g);
+            }
             l0 += nlev;
         }
     };
     build(parse(std::getenv("REXP_FUSE_UP"), "2,2"), false, ft_up);
+    if (rc) return rc;
     build(parse(std::getenv("REXP_FUSE_DOWN"), "2,2"), true, ft_down);
-    return REXP_OK;
+    return rc;
+}
+
+// operators -> the fused kernels' chunked, padded images (after upload_ops)
+int DeviceStore::pack_fused() {
+    if (ft_packed) return REXP_OK;
+    for (int down = 0; down < 2; ++down)
+        for (FtGroup& g : (down ? ft_down : ft_up)) {
+            FtArgs a = g.args;
+            for (int l = 0; l < g.nlev; ++l) {
+                const Level& D = levels[g.l0 + l];
+                a.lv[l].X = D.X; a.lv[l].Y = D.Y; a.lv[l].S = D.S;
+            }
+            ft_pack(a, down != 0, g.img, nh, nullptr);
+        }
+    cudaDeviceSynchronize();
+    ft_packed = true;
+    return check("pack_fused");
 }
 
 const DeviceStore::FtGroup* DeviceStore::ft_group(const std::vector<FtGroup>& v, int l0) const {
@@ -1930,6 +1968,10 @@ const DeviceStore::FtGroup* DeviceStore::ft_group(const std::vector<FtGroup>& v,
 }
 
 int DeviceStore::launch_fused(const FtGroup& g, bool down, int m0, int pc, cudaStream_t s) {
+    if (!ft_packed) {
+        const int rc = pack_fused();
+        if (rc) return rc;
+    }
     FtArgs a = g.args;
     for (int l = 0; l < g.nlev; ++l) {
         const Level& D = levels[g.l0 + l];
@@ -1939,6 +1981,7 @@ int DeviceStore::launch_fused(const FtGroup& g, bool down, int m0, int pc, cudaS
         F.S = D.S + static_cast<size_t>(m0) * D.ppS;
         F.w3 = D.w3;
     }
+    a.img = g.img + static_cast<size_t>(m0) * a.img_ps;
     const int hb = h_sel >= 0 ? h_sel : g.l0 % 2;
     a.hin = d_h[hb];
     a.hout = d_h[hb ^ 1];
@@ -1955,6 +1998,11 @@ int DeviceStore::launch_fused(const FtGroup& g, bool down, int m0, int pc, cudaS
 // real buffers and keep the fastest: DMMA GEMM tiles MT in {2, 4} x WN in
 // {2, 4, 8} (shared store) and the GEMV kernel (nrhs <= 4)
 int DeviceStore::tune_stages(bool measure) {
+    if (measure) {   // called after the operator upload
+        ft_packed = false;
+        const int rc = pack_fused();
+        if (rc) return rc;
+    }
     const size_t nl = levels.size();
     t_upx.assign(nl, StageCfg());
     t_upy.assign(nl, StageCfg());

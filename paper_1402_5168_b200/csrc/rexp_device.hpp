@@ -130,11 +130,13 @@ class DeviceStore {
     private:
     std::vector<StageCfg> t_upx, t_upy, t_down;
     // fused subtree sweeps (fused_tree.cu): groups of consecutive levels run by one kernel
-    struct FtGroup { int l0 = 0, nlev = 0; FtArgs args; };
+    struct FtGroup { int l0 = 0, nlev = 0; FtArgs args; double2* img = nullptr; };
     std::vector<FtGroup> ft_up, ft_down;   // by lowest level, ascending
     std::string ft_times;                  // autotuner: fused vs single-level times
     int h_sel = -1;                        // h buffer holding the current children (-1: by level parity)
-    int plan_fused();
+    int plan_fused(const Tree& T);
+    int pack_fused();
+    bool ft_packed = false;
     const FtGroup* ft_group(const std::vector<FtGroup>& v, int l0) const;
     int launch_fused(const FtGroup& g, bool down, int m0, int pc, cudaStream_t s);
     StageCfg t_root;
