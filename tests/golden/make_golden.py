@@ -22,6 +22,9 @@ Cases (DESIGN.md §9 "Full-size parity"):
   c2s, c4s  BASELINE configs 2 and 4 at full mesh: the resolvent of two
        sampled half poles applied to Re(u0) and Im(u0), at sampled nodes (the
        pole-sharded GPU runs are checked pole by pole).
+  c3s  BASELINE config 3 at full mesh: the same two-sampled-half-pole
+       resolvents for the first and the last of the 64 right-hand sides
+       (seed + 10k, k = 0 and 63): the 64-RHS (R2 = 128) kernels pole by pole.
 """
 from __future__ import annotations
 
@@ -52,6 +55,7 @@ CASES = {
     "c3": "c3_rsw_32x32_p16_x64",
     "c2s": "c2_wave_32x32_p16",
     "c4s": "c4_wave_64x64_p12",
+    "c3s": "c3_rsw_32x32_p16_x64",
 }
 
 _G = {}
@@ -136,8 +140,13 @@ def run(case, procs):
             half = [k for k in range(len(op.poles)) if op.poles[k].imag >= 0]
             mags = np.array([abs(op.res[k]) for k in half])
             picks = [int(np.argmax(mags)), int(np.argmin(np.abs(mags - 1e-2 * mags.max())))]
-            u0 = initial_state(cfg["model"], m.x, m.y, cfg["seed"])
-            parts = np.stack([u0.real.astype(complex), u0.imag.astype(complex)])
+            rhs = [0, cfg["nrhs"] - 1] if case == "c3s" else [0]
+            meta["rhs"] = np.array(rhs)
+            parts = []
+            for k in rhs:
+                u0 = initial_state(cfg["model"], m.x, m.y, cfg["seed"] + 10 * k)
+                parts += [u0.real.astype(complex), u0.imag.astype(complex)]
+            parts = np.stack(parts)
             path = f"/tmp/golden_{case}_parts.npy"
             np.save(path, parts)
             res = dict(pool.imap(_resolvent_only, [(half[j], path) for j in picks], chunksize=1))

@@ -40,12 +40,13 @@ for k in picks:
     eta = x_full[2] * cfg["tau"]
     F = B @ eta
     x = lu.solve(F)
-    # residual in long double (complex as two long double parts)
-    Bl_r, Bl_i = B.real.astype(np.longdouble), B.imag.astype(np.longdouble)
-    xr, xi = x.real.astype(np.longdouble), x.imag.astype(np.longdouble)
-    rr = F.real.astype(np.longdouble) - (Bl_r @ xr - Bl_i @ xi)
-    ri = F.imag.astype(np.longdouble) - (Bl_r @ xi + Bl_i @ xr)
-    r = rr.astype(float) + 1j * ri.astype(float)
+    # residual in long double: CSR products and row sums done by hand (scipy has no long double kernels)
+    ld = np.longdouble
+    dr, di = B.data.real.astype(ld), B.data.imag.astype(ld)
+    xr, xi = x.real.astype(ld)[B.indices], x.imag.astype(ld)[B.indices]
+    pr = np.add.reduceat(dr * xr - di * xi, B.indptr[:-1])
+    pi = np.add.reduceat(dr * xi + di * xr, B.indptr[:-1])
+    r = (F.real.astype(ld) - pr).astype(float) + 1j * (F.imag.astype(ld) - pi).astype(float)
     dx = lu.solve(r)
     rel = np.linalg.norm(dx) / np.linalg.norm(x)
     w = abs(op.res[k]) * np.linalg.norm(dx) / cfg["tau"]
