@@ -1661,6 +1661,14 @@ void DeviceStore::configure_kernels() {
     cudaFuncSetAttribute(k_root_fourier, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cgs_allow();
     ft_allow();
+    cudaFuncSetAttribute(k_spec_pre_fused_b<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_spec_pre_fused_b<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_spec_back_b<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_spec_back_b<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    {
+        const char* env = std::getenv("REXP_SPEC_BATCH");
+        spec_batch = !(env && std::string(env) == "0");
+    }
     lg_allow();
     allow_all<2>();
     allow_all<4>();
@@ -2379,7 +2387,12 @@ int DeviceStore::solve_sum(const double* d_state, double* d_E_out, cudaStream_t 
         SpecArgs sp = spec_args(0, chunk);
         sp.u = d_state; sp.elem_g = d_elem_g; sp.Dm = d_D;
         tbeg(s);
-        k_spec_pre_fused<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
+        if (!spec_batch)
+            k_spec_pre_fused<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
+        else if (R2 % 4 == 0)
+            k_spec_pre_fused_b<4><<<static_cast<unsigned>(nelem * (R2 / 4)), SP_THREADS, sp_pre_smem<4>(p, q), s>>>(sp);
+        else
+            k_spec_pre_fused_b<2><<<static_cast<unsigned>(nelem * (R2 / 2)), SP_THREADS, sp_pre_smem<2>(p, q), s>>>(sp);
         tend(T_PRE, s);
     } else {
         PreArgs a{};
@@ -2418,7 +2431,12 @@ int DeviceStore::solve_sum(const double* d_state, double* d_E_out, cudaStream_t 
         sp.Eedge = d_Eedge;
         sp.E = d_E_out;
         tbeg(s);
-        k_spec_back<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
+        if (!spec_batch)
+            k_spec_back<<<static_cast<unsigned>(nelem * R2), SP_THREADS, 0, s>>>(sp);
+        else if (R2 % 4 == 0)
+            k_spec_back_b<4><<<static_cast<unsigned>(nelem * (R2 / 4)), SP_THREADS, sp_back_smem<4>(q), s>>>(sp);
+        else
+            k_spec_back_b<2><<<static_cast<unsigned>(nelem * (R2 / 2)), SP_THREADS, sp_back_smem<2>(q), s>>>(sp);
         tend(T_POLE_SUM, s);
         return check("spec_back");
     }

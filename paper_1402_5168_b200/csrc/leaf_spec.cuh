@@ -186,5 +186,140 @@ __global__ void __launch_bounds__(SP_THREADS) k_spec_back(SpecArgs a) {
     }
 }
 
+// --------------------------------------------------------------------------
+// Batched forms of the two once-per-step transforms (round 2): one CTA owns a
+// leaf and RB consecutive real right-hand sides (thread = (slot, r), r fastest),
+// so the state is read as whole complex values (16 B, node-fastest), G / E^ /
+// Eedge are accessed in RB x 8-byte runs and E is written node-fastest - the
+// one-(leaf, RHS) kernels above touch one 8-byte word per 32-byte sector
+// (k_spec_pre_fused 0.41 TB/s, k_spec_back 0.55 TB/s on config 3,
+// profiles/r02b_launches_c3.csv).  Dynamic shared memory: sp_pre_smem / sp_back_smem.
+// --------------------------------------------------------------------------
+template <int RB>
+__host__ __device__ constexpr size_t sp_pre_smem(int p, int q) {
+    return (size_t)(3 * p * p * RB + 3 * q * q * RB + SP_T * (SP_T + 1) + p * p) * sizeof(double);
+}
+template <int RB>
+__global__ void __launch_bounds__(SP_THREADS) k_spec_pre_fused_b(SpecArgs a) {
+    extern __shared__ double spsm[];
+    const int q = a.q, p = a.p, q2 = q * q, pp = p * p, t = threadIdx.x;
+    double* us = spsm;                       // [3][pp][RB]; reused as ts [3][q2][RB]
+    double* fs = us + 3 * pp * RB;           // [3][q2][RB]
+    double* vis = fs + 3 * q2 * RB;          // [16][17]
+    double* ds = vis + SP_T * (SP_T + 1);    // [pp]
+    const int nrb = a.R2 / RB;
+    const int leaf = blockIdx.x / nrb, r20 = (blockIdx.x % nrb) * RB;
+    constexpr int NS = SP_THREADS / RB;      // slots
+    const int r = t % RB, slot = t / RB;
+    for (int e = t; e < SP_T * SP_T; e += SP_THREADS) vis[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.Vinv[e];
+    for (int e = t; e < pp; e += SP_THREADS) ds[e] = a.Dm[e];
+    // whole complex values: (c, fld, node), node fastest
+    for (int e = t; e < (RB / 2) * 3 * pp; e += SP_THREADS) {
+        const int node = e % pp, fld = (e / pp) % 3, c = e / (3 * pp);
+        const int g = a.elem_g[(size_t)leaf * pp + node];
+        double2 v = make_double2(0.0, 0.0);
+        if (g >= 0) v = reinterpret_cast<const double2*>(a.u)[((size_t)(r20 / 2 + c) * 3 + fld) * a.N + g];
+        us[(fld * pp + node) * RB + 2 * c] = v.x;
+        us[(fld * pp + node) * RB + 2 * c + 1] = v.y;
+    }
+    __syncthreads();
+    for (int e = slot; e < q2; e += NS) {
+        const int i = e % q + 1, j = e / q + 1;
+        double dx0 = 0.0, dx1 = 0.0, dy0 = 0.0, dy1 = 0.0;
+        for (int kk = 0; kk < p; ++kk) {
+            const double dxw = ds[i * p + kk], dyw = ds[j * p + kk];
+            dx0 = fma(dxw, us[(0 * pp + j * p + kk) * RB + r], dx0);
+            dx1 = fma(dxw, us[(1 * pp + j * p + kk) * RB + r], dx1);
+            dy0 = fma(dyw, us[(0 * pp + kk * p + i) * RB + r], dy0);
+            dy1 = fma(dyw, us[(1 * pp + kk * p + i) * RB + r], dy1);
+        }
+        fs[(0 * q2 + e) * RB + r] = us[(2 * pp + j * p + i) * RB + r];
+        fs[(1 * q2 + e) * RB + r] = a.c1 * (dx0 + dy1);
+        fs[(2 * q2 + e) * RB + r] = a.c1 * (dx1 - dy0);
+    }
+    __syncthreads();
+    double* ts = us;
+    for (int e = slot; e < 3 * q2; e += NS) {
+        const int f = e / q2, node = e % q2, ip = node % q, j = node / q;
+        double sum = 0.0;
+        for (int i = 0; i < q; ++i) sum = fma(vis[ip * (SP_T + 1) + i], fs[(f * q2 + j * q + i) * RB + r], sum);
+        ts[(f * q2 + j * q + ip) * RB + r] = sum;
+    }
+    __syncthreads();
+    for (int e = slot; e < 3 * q2; e += NS) {
+        const int f = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
+        double sum = 0.0;
+        for (int j = 0; j < q; ++j) sum = fma(ts[(f * q2 + j * q + ip) * RB + r], vis[jp * (SP_T + 1) + j], sum);
+        a.G[((size_t)(f * q + ip) * q + jp) * ((size_t)a.nelem * a.R2) + (size_t)leaf * a.R2 + r20 + r] = sum;
+    }
+}
+
+template <int RB>
+__host__ __device__ constexpr size_t sp_back_smem(int q) {
+    return (size_t)(2 * 3 * q * q * RB + SP_T * (SP_T + 1) + 3 * SP_NB * RB) * sizeof(double);
+}
+template <int RB>
+__global__ void __launch_bounds__(SP_THREADS) k_spec_back_b(SpecArgs a) {
+    extern __shared__ double spsm[];
+    const int q = a.q, q2 = q * q, nbnd = 4 * q, t = threadIdx.x;
+    double* es = spsm;                       // [3][q2][RB]; reused as the output tile [3][RB][q2]
+    double* ts = es + 3 * q2 * RB;           // [3][q2][RB]
+    double* vs = ts + 3 * q2 * RB;           // [16][17]
+    double* eb = vs + SP_T * (SP_T + 1);     // [3][SP_NB][RB]
+    const int nrb = a.R2 / RB;
+    const int leaf = blockIdx.x / nrb, r20 = (blockIdx.x % nrb) * RB;
+    constexpr int NS = SP_THREADS / RB;
+    const int r = t % RB, slot = t / RB;
+    const size_t ncol = (size_t)a.nelem * a.R2, col = (size_t)leaf * a.R2 + r20 + r;
+    for (int e = t; e < SP_T * SP_T; e += SP_THREADS) vs[(e / SP_T) * (SP_T + 1) + e % SP_T] = a.V[e];
+    for (int e = slot; e < a.nE * q2; e += NS) {
+        const int kk = e / q2, mode = e % q2, ip = mode % q, jp = mode / q;
+        const double* src = a.Ehat + ((size_t)(kk * q + ip) * q + jp) * ncol + col;
+        double s = 0.0;
+        for (int gi = 0; gi < 2 * a.ngroups; ++gi) s += src[(size_t)gi * a.nE * q2 * ncol];
+        const double* G = a.G + ((size_t)ip * q + jp) * ncol + col;
+        for (int f = 0; f < a.nF; ++f)
+            s += a.Pi[((size_t)kk * a.nF + f) * SP_T * SP_T + ip * SP_T + jp] * G[(size_t)f * q2 * ncol];
+        es[(kk * q2 + mode) * RB + r] = s;
+    }
+    for (int e = slot; e < a.nE * nbnd; e += NS) {
+        const int kk = e / nbnd, b = e % nbnd;
+        double s = 0.0;
+        if (a.own[(size_t)leaf * nbnd + b]) {
+            const double* src = a.Eedge + ((size_t)kk * a.NE + a.gB[(size_t)leaf * nbnd + b]) * a.R2 + r20 + r;
+            for (int gi = 0; gi < a.ngroups; ++gi) s += src[(size_t)gi * a.nE * a.NE * a.R2];
+        }
+        eb[(kk * SP_NB + b) * RB + r] = s;
+    }
+    __syncthreads();
+    for (int e = slot; e < a.nE * nbnd; e += NS) {
+        const int kk = e / nbnd, b = e % nbnd;
+        if (!a.own[(size_t)leaf * nbnd + b]) continue;
+        const int side = b / q, s1 = b % q;
+        double s = 0.0;
+        for (int kq = 0; kq < q; ++kq) s = fma(vs[s1 * (SP_T + 1) + kq], eb[(kk * SP_NB + side * q + kq) * RB + r], s);
+        a.E[((size_t)kk * a.R2 + r20 + r) * a.N + (a.N - a.NE) + a.gB[(size_t)leaf * nbnd + b]] = s;
+    }
+    for (int e = slot; e < a.nE * q2; e += NS) {
+        const int kk = e / q2, node = e % q2, i = node % q, jp = node / q;
+        double s = 0.0;
+        for (int ipp = 0; ipp < q; ++ipp) s = fma(vs[i * (SP_T + 1) + ipp], es[(kk * q2 + jp * q + ipp) * RB + r], s);
+        ts[(kk * q2 + jp * q + i) * RB + r] = s;
+    }
+    __syncthreads();
+    double* out = es;                        // [3][RB][q2]
+    for (int e = slot; e < a.nE * q2; e += NS) {
+        const int kk = e / q2, node = e % q2, i = node % q, j = node / q;
+        double s = 0.0;
+        for (int jpp = 0; jpp < q; ++jpp) s = fma(ts[(kk * q2 + jpp * q + i) * RB + r], vs[j * (SP_T + 1) + jpp], s);
+        out[(kk * RB + r) * q2 + node] = s;
+    }
+    __syncthreads();
+    for (int e = t; e < a.nE * RB * q2; e += SP_THREADS) {
+        const int node = e % q2, rr = (e / q2) % RB, kk = e / (q2 * RB);
+        a.E[((size_t)kk * a.R2 + r20 + rr) * a.N + (size_t)leaf * q2 + node] = out[e];
+    }
+}
+
 }  // namespace dev
 }  // namespace rexp

@@ -137,6 +137,7 @@ class DeviceStore {
     int plan_fused(const Tree& T);
     int pack_fused();
     bool ft_packed = false;
+    bool spec_batch = true;                // batched k_spec_pre_fused_b / k_spec_back_b (REXP_SPEC_BATCH=0: one (leaf, RHS) per CTA)
     const FtGroup* ft_group(const std::vector<FtGroup>& v, int l0) const;
     int launch_fused(const FtGroup& g, bool down, int m0, int pc, cudaStream_t s);
     StageCfg t_root;
