@@ -10,7 +10,7 @@ template <int MT, int WN, int BK, int R2T, int MODE, int NST, bool PF>
 void cgs_launch(dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
     constexpr int WM = WN == 2 ? 4 : WN == 4 ? 2 : 1;
     k_cgemm_sym<MT, WN, BK, R2T, MODE, WM, NST, PF>
-        <<<grid, 32 * WN * WM, cgemm_sym_smem_bytes<MT, WN, BK, WM, NST>(), s>>>(a);
+        <<<grid, 32 * WN * WM, cgemm_sym_smem_bytes<MT, WN, BK, WM, NST, MODE>(), s>>>(a);
 }
 template <int MT, int WN, int BK, int R2T, int MODE, int NST, bool PF>
 void cgs_allow1() {
@@ -56,6 +56,13 @@ void cgs_tiles(int MT, int WN, int nst, bool pf, dim3 grid, cudaStream_t s, cons
             return;
         }
     }
+    // UP-X single-stage cp.async ring (both children's gathers copied raw), R2 = 128
+    if constexpr (MODE == CG_UPX && R2T == 128) {
+        if (nst == 11) {
+            cgs_tiles_n<BK, R2T, MODE, 11, false>(MT, WN, grid, s, a);
+            return;
+        }
+    }
     cgs_tiles_n<BK, R2T, MODE, 2, false>(MT, WN, grid, s, a);
 }
 template <int BK, int R2T, int MODE, int NST, bool PF>
@@ -68,6 +75,7 @@ template <int BK, int R2T, int MODE>
 void cgs_allow_tiles() {
     cgs_allow_n<BK, R2T, MODE, 2, false>();
     if constexpr (MODE == CG_UPY || MODE == CG_DOWN) cgs_allow_n<BK, R2T, MODE, 3, false>();
+    if constexpr (MODE == CG_UPX && R2T == 128) cgs_allow_n<BK, R2T, MODE, 11, false>();
     if constexpr (cgs_has_pf<R2T, MODE>()) {
         cgs_allow_n<BK, R2T, MODE, 2, true>();
         cgs_allow_n<BK, R2T, MODE, 3, true>();

@@ -131,9 +131,11 @@ __device__ __forceinline__ void cgs_epilogue(const CgemmSymArgs& s, int m, int r
 // CTAs per SM for the short-K, latency-bound low levels)
 template <int NST>
 __host__ __device__ constexpr int cgs_ring() { return NST >= 10 ? NST - 10 : NST; }
-template <int MT, int WN, int BK, int WM = 1, int NST = 2>
+template <int MT, int WN, int BK, int WM = 1, int NST = 2, int MODE = CG_UPY>
 __host__ __device__ constexpr size_t cgemm_sym_smem_bytes() {
-    return (size_t)cgs_ring<NST>() * 2 * BK * ((8 * MT * WM + 2) + (8 * WN + 2)) * sizeof(double2);
+    // the UP-X ring stages both children's raw gathers of x_A and x_B (4 tiles per stage)
+    constexpr int XT = (MODE == CG_UPX && NST >= 10) ? 2 : 1;
+    return (size_t)cgs_ring<NST>() * 2 * BK * ((8 * MT * WM + 2) + XT * (8 * WN + 2)) * sizeof(double2);
 }
 
 // gathered source address of x at full input position pos (UP-Y, DOWN: one 16-byte value)
@@ -170,11 +172,13 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
     const double2* Ap = a.A + (size_t)m * 2 * hr * hk;   // M+
     const double2* Am = Ap + (size_t)hr * hk;            // M-
 
-    if constexpr (NST >= 3 && (MODE == CG_UPY || MODE == CG_DOWN)) {
+    constexpr bool kRingX = MODE == CG_UPX && NST >= 10;   // UP-X: h^a_3 and h^b_3 copied raw, summed in the loop
+    if constexpr (NST >= 3 && (MODE == CG_UPY || MODE == CG_DOWN || kRingX)) {
         // ring of RS stages: [stage][half] A tiles, then [stage][A|B] raw x tiles
         constexpr int RS = cgs_ring<NST>();
         auto AsN = [&](int st, int hf) { return sm + (st * 2 + hf) * BK * LDA; };
         auto XsN = [&](int st, int ab) { return sm + RS * 2 * BK * LDA + (st * 2 + ab) * BK * LDB; };
+        auto XsN2 = [&](int st, int ab) { return sm + RS * 2 * BK * (LDA + LDB) + (st * 2 + ab) * BK * LDB; };
         auto issue = [&](int st, int k0) {
             for (int e = tid; e < 2 * BK * BM; e += NT) {
                 const int hf = e / (BK * BM), ee = e % (BK * BM);
@@ -190,10 +194,24 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                 const int kk = ee / BN, c = ee % BN;
                 const int k = k0 + kk, col = col0 + c;
                 double2* base = XsN(st, ab);
-                if (k < hk && col < ncols)
-                    cp_async16(base + kk * LDB + c,
-                               cgs_src<R2T, MODE>(s, m, ab ? s.iB[k] : s.iA[k], col / R2, col % R2));
-                else base[kk * LDB + c] = make_double2(0.0, 0.0);
+                if constexpr (kRingX) {
+                    double2* base2 = XsN2(st, ab);
+                    if (k < hk && col < ncols) {
+                        const int pos = ab ? s.iB[k] : s.iA[k], node = col / R2, r2 = col % R2;
+                        const double2* srcm = a.src + (size_t)m * a.src_ps * R2;
+                        const int cbase = cg_child_base(a, node);
+                        cp_async16(base + kk * LDB + c, srcm + (size_t)(cbase + a.bi0[pos]) * R2 + r2);
+                        cp_async16(base2 + kk * LDB + c, srcm + (size_t)(cbase + a.bi1[pos]) * R2 + r2);
+                    } else {
+                        base[kk * LDB + c] = make_double2(0.0, 0.0);
+                        base2[kk * LDB + c] = make_double2(0.0, 0.0);
+                    }
+                } else {
+                    if (k < hk && col < ncols)
+                        cp_async16(base + kk * LDB + c,
+                                   cgs_src<R2T, MODE>(s, m, ab ? s.iB[k] : s.iA[k], col / R2, col % R2));
+                    else base[kk * LDB + c] = make_double2(0.0, 0.0);
+                }
             }
             cp_async_commit();
         };
@@ -234,7 +252,12 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                 const int kk = ks * 4 + t4;
                 const int k = ch * BK + kk;
                 const double sg = k < hk ? __ldg(s.is + k) : 0.0;
-                const double2 xa = XA[kk * LDB + warp * 8 + g], xb = XB[kk * LDB + warp * 8 + g];
+                double2 xa = XA[kk * LDB + warp * 8 + g], xb = XB[kk * LDB + warp * 8 + g];
+                if constexpr (kRingX) {
+                    const double2 xa2 = XsN2(st, 0)[kk * LDB + warp * 8 + g], xb2 = XsN2(st, 1)[kk * LDB + warp * 8 + g];
+                    xa.x += xa2.x; xa.y += xa2.y;
+                    xb.x += xb2.x; xb.y += xb2.y;
+                }
                 const double2 bp = make_double2(xa.x + sg * xb.x, xa.y + sg * xb.y);
                 const double2 bm = make_double2(xa.x - sg * xb.x, xa.y - sg * xb.y);
 #pragma unroll

@@ -2034,6 +2034,12 @@ int DeviceStore::tune_stages(bool measure) {
         // test hook: REXP_GEMM_STAGES=3 forces the 3-stage cp.async GEMM on every
         // UP-Y / DOWN stage that runs as a GEMM (no autotuning)
         const char* st = std::getenv("REXP_GEMM_STAGES");
+        if (st && std::string(st) == "x1") {
+            // UP-X single-stage cp.async ring (compiled for R2 = 128) on every pair-GEMM level
+            for (size_t li = 0; li < nl; ++li)
+                if (t_upx[li].kind == 3 && R2 == 128) t_upx[li].minb = 6;
+            return REXP_OK;
+        }
         if (st && std::string(st) == "3") {
             for (size_t li = 0; li < nl; ++li) {
                 if (t_upy[li].kind == 0 || t_upy[li].kind == 3) t_upy[li].minb = 3;
@@ -2091,7 +2097,8 @@ int DeviceStore::tune_stages(bool measure) {
             // minb low bits: 1 register-staged B, 3 / 5 / 6 cp.async ring of 3 / 2 / 1 stage(s)
             for (int nst : {1, 3, 5, 6})
                 for (int pf : {0, 32}) {
-                    if (nst != 1 && kind == 0) continue;   // rings: plain-gather modes (UP-Y, DOWN)
+                    // rings: plain-gather modes (UP-Y, DOWN); UP-X only as the single-stage ring at R2 = 128
+                    if (nst != 1 && kind == 0 && !(nst == 6 && R2 == 128)) continue;
                     if ((nst == 5 || nst == 6) && R2 != 128) continue;
                     if (pf && (kind == 0 || R2 != 128)) continue;   // prefetched epilogue terms: UP-Y / DOWN, R2 = 128
                     for (int mt : {2, 4})

@@ -152,7 +152,7 @@ def test_config0_three_stage_gemm(c0, nrhs, monkeypatch):
     h.close()
 
 
-@pytest.mark.parametrize("nrhs,stages", [(8, "tuned"), (8, "3"), (64, "tuned")])
+@pytest.mark.parametrize("nrhs,stages", [(8, "tuned"), (8, "3"), (64, "tuned"), (64, "x1")])
 def test_config0_symmetric_pair_gemm_many_rhs(c0, nrhs, stages, monkeypatch):
     """nrhs = 8 (R2 = 16, runtime R2) and 64 (R2 = 128, config 3's RHS count,
     compile-time R2): every merge level above the first runs as the
@@ -161,13 +161,15 @@ def test_config0_symmetric_pair_gemm_many_rhs(c0, nrhs, stages, monkeypatch):
     (nrhs/8)-th RHS against the oracle: the RHS are independent)."""
     cfg, m, op, u0 = c0
     Lam = cfg["Lambda_tau"] / cfg["tau"]
-    if stages == "3":
-        monkeypatch.setenv("REXP_GEMM_STAGES", "3")
+    if stages in ("3", "x1"):   # "x1": the single-stage cp.async ring of the up-X pair GEMM (R2 = 128)
+        monkeypatch.setenv("REXP_GEMM_STAGES", stages)
     U = np.stack([rsw_initial_state(m.x, m.y, cfg["seed"] + 10 * k) for k in range(nrhs)])
     h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], nrhs=nrhs)
     assert "symgemm" in h.stage_report
     if stages == "3":
         assert "s3" in h.stage_report
+    if stages == "x1":
+        assert "s1" in h.stage_report
     got = _gpu_apply(h, U, 2)
     errs = [rel_l2(got[k], op.evolve(U[k], 2)) for k in range(0, nrhs, nrhs // 8)]
     print(f"symmetric-pair GEMM nrhs {nrhs}: max rel L2 {max(errs):.3e}")
