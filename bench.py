@@ -117,7 +117,7 @@ def tree_dims(n, q):
         lev += 1
 
 
-def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
+def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3, sym2=False):
     """Algorithmic FP64 flops and operator bytes per step, per kernel class.
     Complex multiply-add = 8 flops, complex x real multiply-add = 4, complex
     product = 6; operator element = 16 bytes.  leaf = "spectral" counts the
@@ -143,15 +143,19 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3):
     sym = shared and leaf == "spectral"
     lv = [(nd, n3, nx, 0.5 if (sym and i > 0 and (nd * R2 <= 8 or R2 >= 16)) else 1.0)
           for i, (nd, n3, nx) in enumerate(lv)]
+    # second reflection (device.cu: sym_pairs2, R2 >= 16): Y keeps half of the pair form's
+    # rows and S half of its columns
+    h2 = 0.5 if (sym2 and R2 >= 16) else 1.0
+    y2 = lambda hf: hf * (h2 if hf < 1.0 else 1.0)
     merge = {
-        "merge_up": (sum(hf * nh * nd * (n3 * n3 + nx * n3) * R2 * 8 for nd, n3, nx, hf in lv),
-                     sum(hf * nh * per(nd) * (n3 * n3 + nx * n3) * 16 for nd, n3, nx, hf in lv)),
+        "merge_up": (sum(nh * nd * (hf * n3 * n3 + y2(hf) * nx * n3) * R2 * 8 for nd, n3, nx, hf in lv),
+                     sum(nh * per(nd) * (hf * n3 * n3 + y2(hf) * nx * n3) * 16 for nd, n3, nx, hf in lv)),
         # shared store: Fourier root (two DFTs over the n elements of the 2nq seam
         # unknowns, n blocks of (2q)^2); per-node: dense (2nq)^2
         "root": ((nh * R2 * (2 * 2 * n * q * n * 8 + n * (2 * q) ** 2 * 8), nh * n * (2 * q) ** 2 * 16) if shared
                  else (nh * (2 * n * q) ** 2 * R2 * 8, nh * (2 * n * q) ** 2 * 16)),
-        "merge_down": (sum(hf * nh * nd * n3 * nx * R2 * 8 for nd, n3, nx, hf in lv),
-                       sum(hf * nh * per(nd) * n3 * nx * 16 for nd, n3, nx, hf in lv)),
+        "merge_down": (sum(y2(hf) * nh * nd * n3 * nx * R2 * 8 for nd, n3, nx, hf in lv),
+                       sum(y2(hf) * nh * per(nd) * n3 * nx * 16 for nd, n3, nx, hf in lv)),
     }
     if leaf == "spectral":
         unit = nh * e * R2
@@ -222,7 +226,8 @@ def roofline_for(cfg, workload, h, times, steps, pk, step_ms, nh_here=None):
     R2 = 2 * h.nrhs
     shared = (cfg["model"] == "rsw")
     nF, nE = (3, 3) if cfg["model"] == "rsw" else (2, 2)
-    work = class_work(cfg, nh, R2, shared, leaf=h.leaf_solver or "dense", nF=nF, nE=nE)
+    work = class_work(cfg, nh, R2, shared, leaf=h.leaf_solver or "dense", nF=nF, nE=nE,
+                      sym2="sym2[" in (h.stage_report or ""))
     sbytes = state_bytes(cfg, nh, R2, shared, nF, nE)
     hbm = pk.get("hbm_gbs", 6549.8)
     total_ms = sum(t for t, c in times.values())
@@ -314,8 +319,8 @@ def oracle_sample(cfg, npoles_sample=None, nrhs_sample=2):
     dof = 3 * m.N * cfg["nrhs"]
     return {"value": dof / step_s, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{len(idx)} of {P} poles x {nr} of {cfg['nrhs']} RHS on the full "
-                      f"{cfg['n']}x{cfg['n']}x{cfg['p']}^2 mesh, one resolvent apply each (scipy splu, "
-                      f"single-threaded; factor untimed, {factor_s:.1f}s), step time extrapolated "
+                      f"{cfg['n']}x{cfg['n']}x{cfg['p']}^2 mesh, one resolvent apply each (scipy splu + two "
+                      f"refinement steps, single-threaded; factor untimed, {factor_s:.1f}s), step time extrapolated "
                       f"x{P}/{len(idx)} poles x{cfg['nrhs']}/{nr} RHS",
             "step_seconds": step_s}
 

@@ -9,8 +9,17 @@ namespace {
 template <int MT, int WN, int BK, int R2T, int MODE, int NST, bool PF>
 void cgs_launch(dim3 grid, cudaStream_t s, const CgemmSymArgs& a) {
     constexpr int WM = WN == 2 ? 4 : WN == 4 ? 2 : 1;
-    k_cgemm_sym<MT, WN, BK, R2T, MODE, WM, NST, PF>
-        <<<grid, 32 * WN * WM, cgemm_sym_smem_bytes<MT, WN, BK, WM, NST, MODE>(), s>>>(a);
+    size_t smem = cgemm_sym_smem_bytes<MT, WN, BK, WM, NST, MODE>();
+    // DOWN rings with the second reflection stage the partners' raw tiles too
+    if (MODE == CG_DOWN && NST >= 3 && a.sym2) smem += (size_t)cgs_ring<NST>() * 2 * BK * (8 * WN + 2) * sizeof(double2);
+    if constexpr (NST != 2) {
+        // a ring that does not fit (3 stages of a wide tile plus the partner tiles): register-staged form
+        if (smem > 200 * 1024) {
+            cgs_launch<MT, WN, BK, R2T, MODE, 2, false>(grid, s, a);
+            return;
+        }
+    }
+    k_cgemm_sym<MT, WN, BK, R2T, MODE, WM, NST, PF><<<grid, 32 * WN * WM, smem, s>>>(a);
 }
 template <int MT, int WN, int BK, int R2T, int MODE, int NST, bool PF>
 void cgs_allow1() {

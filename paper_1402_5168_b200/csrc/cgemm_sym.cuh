@@ -24,6 +24,11 @@ struct CgemmSymArgs {
     const int *oA, *oB;       // output pairs (rows)
     const double* os;
     int n3, next;             // full interface / boundary sizes of the level
+    // second reflection (device.cu: sym_pairs2): partners of the boundary pairs and their signs;
+    // UP-Y writes them too, DOWN adds them to the gathered operand (-1: the pair has no partner)
+    int sym2;
+    const int *xA2, *xB2;
+    const double *xsA2, *xsB2;
 };
 
 struct BRawSym { double v[8]; };
@@ -31,7 +36,8 @@ struct BRawSym { double v[8]; };
 // x at full input position pos for column col: UPX s3 = h^a_3 + h^b_3 (two gathers),
 // UPY w3, DOWN u_ext
 template <int R2T, int MODE>
-__device__ __forceinline__ void cgs_fetch1(const CgemmSymArgs& s, int m, int pos, int node, int r2, double* out) {
+__device__ __forceinline__ void cgs_fetch1(const CgemmSymArgs& s, int m, int pos, int node, int r2, double* out,
+                                           int pos2 = -1, double sg2 = 0.0) {
     const CgemmArgs& a = s.g;
     const int R2 = R2T ? R2T : a.R2;
     if (MODE == CG_UPX) {
@@ -43,9 +49,13 @@ __device__ __forceinline__ void cgs_fetch1(const CgemmSymArgs& s, int m, int pos
     } else if (MODE == CG_UPY) {
         const double2 v = a.src[(size_t)m * a.src_ps * R2 + ((size_t)node * s.n3 + pos) * R2 + r2];
         out[0] = v.x; out[1] = v.y; out[2] = 0.0; out[3] = 0.0;
-    } else {   // DOWN
+    } else {   // DOWN (+ the reflection-2 partner, summed like UP-X's second child)
         const double2 v = a.src[((size_t)m * a.src_ps + a.bi0[(size_t)node * s.next + pos]) * R2 + r2];
         out[0] = v.x; out[1] = v.y; out[2] = 0.0; out[3] = 0.0;
+        if (pos2 >= 0) {
+            const double2 w = a.src[((size_t)m * a.src_ps + a.bi0[(size_t)node * s.next + pos2]) * R2 + r2];
+            out[2] = sg2 * w.x; out[3] = sg2 * w.y;
+        }
     }
 }
 
@@ -113,6 +123,16 @@ __device__ __forceinline__ void cgs_epilogue(const CgemmSymArgs& s, int m, int r
                 double2* dst = a.dst + (size_t)m * a.dst_ps * R2;
                 dst[((size_t)node * s.next + ra) * R2 + r2] = make_double2(yA.x + ea.x, yA.y + ea.y);
                 dst[((size_t)node * s.next + rbw) * R2 + r2] = make_double2(yB.x + eb.x, yB.y + eb.y);
+                if (s.sym2) {   // the reflection-2 partners carry the same values up to the edge-basis sign
+                    const int pa = s.xA2[rr], pb = s.xB2[rr];
+                    if (pa >= 0) {
+                        const double ga = s.xsA2[rr], gb = s.xsB2[rr];
+                        const double2 fa = a.add[((size_t)m * a.add_ps + base + a.ai0[pa]) * R2 + r2];
+                        const double2 fb = a.add[((size_t)m * a.add_ps + base + a.ai0[pb]) * R2 + r2];
+                        dst[((size_t)node * s.next + pa) * R2 + r2] = make_double2(fma(ga, yA.x, fa.x), fma(ga, yA.y, fa.y));
+                        dst[((size_t)node * s.next + pb) * R2 + r2] = make_double2(fma(gb, yB.x, fb.x), fma(gb, yB.y, fb.y));
+                    }
+                }
             } else {   // DOWN: u3 = y + w3, scattered to the edge array
                 const double2* w3 = a.add + (size_t)m * a.add_ps * R2;
                 const double2 wa = PF ? pre[i][j][0] : w3[((size_t)node * s.n3 + ra) * R2 + r2];
@@ -211,6 +231,12 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                         cp_async16(base + kk * LDB + c,
                                    cgs_src<R2T, MODE>(s, m, ab ? s.iB[k] : s.iA[k], col / R2, col % R2));
                     else base[kk * LDB + c] = make_double2(0.0, 0.0);
+                    if (MODE == CG_DOWN && s.sym2) {   // reflection-2 partner of the gathered value
+                        double2* base2 = XsN2(st, ab);
+                        const int pos2 = (k < hk && col < ncols) ? (ab ? s.xB2[k] : s.xA2[k]) : -1;
+                        if (pos2 >= 0) cp_async16(base2 + kk * LDB + c, cgs_src<R2T, MODE>(s, m, pos2, col / R2, col % R2));
+                        else base2[kk * LDB + c] = make_double2(0.0, 0.0);
+                    }
                 }
             }
             cp_async_commit();
@@ -257,6 +283,12 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
                     const double2 xa2 = XsN2(st, 0)[kk * LDB + warp * 8 + g], xb2 = XsN2(st, 1)[kk * LDB + warp * 8 + g];
                     xa.x += xa2.x; xa.y += xa2.y;
                     xb.x += xb2.x; xb.y += xb2.y;
+                }
+                if (MODE == CG_DOWN && s.sym2) {
+                    const double2 xa2 = XsN2(st, 0)[kk * LDB + warp * 8 + g], xb2 = XsN2(st, 1)[kk * LDB + warp * 8 + g];
+                    const double ga = k < hk ? __ldg(s.xsA2 + k) : 0.0, gb = k < hk ? __ldg(s.xsB2 + k) : 0.0;
+                    xa.x = fma(ga, xa2.x, xa.x); xa.y = fma(ga, xa2.y, xa.y);
+                    xb.x = fma(gb, xb2.x, xb.x); xb.y = fma(gb, xb2.y, xb.y);
                 }
                 const double2 bp = make_double2(xa.x + sg * xb.x, xa.y + sg * xb.y);
                 const double2 bm = make_double2(xa.x - sg * xb.x, xa.y - sg * xb.y);
@@ -324,8 +356,13 @@ __global__ void __launch_bounds__(32 * WN * WM) k_cgemm_sym(CgemmSymArgs s) {
             for (int j = 0; j < 8; ++j) braw[u].v[j] = 0.0;
             if (e < BK * BN && k < hk && col < ncols) {
                 const int node = col / R2, r2 = col % R2;
-                cgs_fetch1<R2T, MODE>(s, m, s.iA[k], node, r2, braw[u].v);
-                cgs_fetch1<R2T, MODE>(s, m, s.iB[k], node, r2, braw[u].v + 4);
+                if (MODE == CG_DOWN && s.sym2) {
+                    cgs_fetch1<R2T, MODE>(s, m, s.iA[k], node, r2, braw[u].v, s.xA2[k], s.xsA2[k]);
+                    cgs_fetch1<R2T, MODE>(s, m, s.iB[k], node, r2, braw[u].v + 4, s.xB2[k], s.xsB2[k]);
+                } else {
+                    cgs_fetch1<R2T, MODE>(s, m, s.iA[k], node, r2, braw[u].v);
+                    cgs_fetch1<R2T, MODE>(s, m, s.iB[k], node, r2, braw[u].v + 4);
+                }
             }
         }
     };

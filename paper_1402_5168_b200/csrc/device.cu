@@ -1315,9 +1315,12 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         // latency-bound low levels of few-RHS runs keep the full GEMM
         if (fdm && li > 0 && (L.nodes * R2 <= 8 || R2 >= 16) && std::getenv("REXP_NO_SYM") == nullptr)
             if ((rc = sym_pairs(T, L, D))) return rc;   // sets D.sym when the pairing is a fixed-point-free involution
+        if (D.sym && R2 >= 16 && std::getenv("REXP_NO_SYM2") == nullptr)
+            if ((rc = sym_pairs2(T, L, D))) return rc;  // sets D.sym2 / D.hx2
+        const size_t hxs = D.sym2 ? static_cast<size_t>(D.hx2) : static_cast<size_t>(L.next / 2);
         D.ppX = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * (L.n3 / 2) : st * L.n3 * L.n3;
-        D.ppY = D.sym ? 2 * static_cast<size_t>(L.next / 2) * (L.n3 / 2) : st * L.next * L.n3;
-        D.ppS = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * (L.next / 2) : st * L.n3 * L.next;
+        D.ppY = D.sym ? 2 * hxs * (L.n3 / 2) : st * L.next * L.n3;
+        D.ppS = D.sym ? 2 * static_cast<size_t>(L.n3 / 2) * hxs : st * L.n3 * L.next;
         if ((rc = alloc(&D.X, nh * D.ppX))) return rc;
         if ((rc = alloc(&D.Y, nh * D.ppY))) return rc;
         if ((rc = alloc(&D.S, nh * D.ppS))) return rc;
@@ -1478,6 +1481,64 @@ int DeviceStore::sym_pairs(const Tree& T, const MergeLevel& L, Level& D) {
     return REXP_OK;
 }
 
+// Second reflection of a pair level: across the interface (x-merge: x -> a H - x,
+// y-merge: y -> b H - y).  It swaps the two (identical, themselves symmetric)
+// children and fixes every interface position, so Y's rows at mirrored boundary
+// positions are equal up to the edge-basis sign (y(R2 p) = sigma_p y(p)) and S's
+// columns likewise (S(., R2 p) = sigma_p S(., p)).  Of each reflection-2 orbit of
+// boundary pairs (A, B) only one is kept: Y is stored / multiplied with hx2 rows,
+// S with hx2 columns; the kernels write (UP-Y) or gather (DOWN) the partners.
+int DeviceStore::sym_pairs2(const Tree& T, const MergeLevel& L, Level& D) {
+    const double H = 1.0 / T.n;
+    auto wrapd = [](double v) { return std::fabs(v - std::floor(v + 0.5)); };
+    const int cnt = L.next, hx = cnt / 2;
+    const int32_t* gl = L.gext.data();
+    std::vector<int> part(cnt, -1);
+    std::vector<double> sg(cnt, 1.0);
+    for (int r = 0; r < cnt; ++r) {
+        const double x = T.x[T.NI + gl[r]], y = T.y[T.NI + gl[r]];
+        const double mx = L.dir == 0 ? L.a * H - x : x, my = L.dir == 0 ? y : L.b * H - y;
+        int rm = -1;
+        for (int u = 0; u < cnt; ++u)
+            if (wrapd(T.x[T.NI + gl[u]] - mx) + wrapd(T.y[T.NI + gl[u]] - my) < 1e-9) { rm = u; break; }
+        if (rm < 0) return REXP_OK;
+        const int k = r % q, km = rm % q;
+        if (km == k) sg[r] = 1.0;
+        else if (km == q - 1 - k) sg[r] = mode_parity[k];
+        else return REXP_OK;
+        part[r] = (rm / q) * q + k;
+    }
+    for (int r = 0; r < cnt; ++r)
+        if (part[r] == r || part[part[r]] != r || sg[part[r]] != sg[r]) return REXP_OK;
+    std::vector<int> half_of(cnt, -1);
+    for (int r = 0; r < hx; ++r) { half_of[D.h_eA[r]] = r; half_of[D.h_eB[r]] = r; }
+    std::vector<char> done(hx, 0);
+    std::vector<int> eA, eB, pA, pB;
+    std::vector<double> es, sA, sB;
+    for (int r = 0; r < hx; ++r) {
+        if (done[r]) continue;
+        const int a = D.h_eA[r], b = D.h_eB[r];
+        const int r2 = half_of[part[a]];
+        if (r2 < 0 || half_of[part[b]] != r2) return REXP_OK;   // the reflections must commute on the pairs
+        done[r] = 1;
+        eA.push_back(a); eB.push_back(b); es.push_back(D.h_es[r]);
+        if (r2 == r) {   // the orbit is the pair itself: nothing to duplicate
+            pA.push_back(-1); pB.push_back(-1); sA.push_back(0.0); sB.push_back(0.0);
+        } else {
+            done[r2] = 1;
+            pA.push_back(part[a]); pB.push_back(part[b]); sA.push_back(sg[a]); sB.push_back(sg[b]);
+        }
+    }
+    int rc;
+    if ((rc = put(&D.e2A, eA)) || (rc = put(&D.e2B, eB)) || (rc = put(&D.e2s, es)) || (rc = put(&D.e2pA, pA)) ||
+        (rc = put(&D.e2pB, pB)) || (rc = put(&D.e2sA, sA)) || (rc = put(&D.e2sB, sB)))
+        return rc;
+    D.h_e2A = eA; D.h_e2B = eB; D.h_e2s = es;
+    D.hx2 = static_cast<int>(eA.size());
+    D.sym2 = true;
+    return REXP_OK;
+}
+
 // copy the host factorization of local half poles [m0, m0 + count) into the store
 int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
     ft_packed = false;   // the fused kernels' operator images are rebuilt from the new store
@@ -1502,7 +1563,10 @@ int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
         if (D.sym) {
             // [M+ | M-] per pole from the full (column-major) X, Y, S:
             //   M+- (r, c) = A(A_r, A_c) +- s_c A(A_r, B_c)
-            const int n3 = D.n3, ne = D.next, h3 = n3 / 2, hx = ne / 2;
+            const int n3 = D.n3, ne = D.next, h3 = n3 / 2, hx = D.sym2 ? D.hx2 : ne / 2;
+            const std::vector<int>& xA = D.sym2 ? D.h_e2A : D.h_eA;
+            const std::vector<int>& xB = D.sym2 ? D.h_e2B : D.h_eB;
+            const std::vector<double>& xs = D.sym2 ? D.h_e2s : D.h_es;
             const HostLevelOps& H = ops[li + 1];
             const size_t npole = H.m[0].size() / (static_cast<size_t>(n3) * n3);
             std::vector<cd> X2(npole * D.ppX), Y2(npole * D.ppY), S2(npole * D.ppS);
@@ -1519,9 +1583,9 @@ int DeviceStore::upload_ops(const std::vector<HostLevelOps>& ops, int m0) {
             };
             for (size_t pl = 0; pl < npole; ++pl) {
                 pair_op(H.m[0].data() + pl * n3 * n3, n3, h3, h3, D.h_iA, D.h_iA, D.h_iB, D.h_is, X2.data() + pl * D.ppX);
-                pair_op(H.m[1].data() + pl * static_cast<size_t>(ne) * n3, ne, hx, h3, D.h_eA, D.h_iA, D.h_iB, D.h_is,
+                pair_op(H.m[1].data() + pl * static_cast<size_t>(ne) * n3, ne, hx, h3, xA, D.h_iA, D.h_iB, D.h_is,
                         Y2.data() + pl * D.ppY);
-                pair_op(H.m[2].data() + pl * static_cast<size_t>(n3) * ne, n3, h3, hx, D.h_iA, D.h_eA, D.h_eB, D.h_es,
+                pair_op(H.m[2].data() + pl * static_cast<size_t>(n3) * ne, n3, h3, hx, D.h_iA, xA, xB, xs,
                         S2.data() + pl * D.ppS);
             }
             if ((rc = up(X2, D.X, D.ppX))) return rc;
@@ -1756,7 +1820,7 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
         CgemmArgs& a = sa.g;
         a.nodes = L.nodes; a.R2 = R2;
         a.nbx = L.nbx; a.xdir = L.dir == 0 ? 1 : 0; a.nchild = L.nchild;
-        const int h3 = L.n3 / 2, hx = L.next / 2;
+        const int h3 = L.n3 / 2, hx = L.sym2 ? L.hx2 : L.next / 2;
         int mode;
         if (kind == 0) {
             mode = CG_UPX;
@@ -1778,6 +1842,12 @@ int DeviceStore::launch_stage(int kind, size_t li, const StageCfg& cfg, int m0, 
         const bool in_int = kind != 2, out_int = kind != 1;
         sa.iA = in_int ? L.siA : L.seA; sa.iB = in_int ? L.siB : L.seB; sa.is = in_int ? L.sis : L.ses;
         sa.oA = out_int ? L.siA : L.seA; sa.oB = out_int ? L.siB : L.seB; sa.os = out_int ? L.sis : L.ses;
+        if (L.sym2) {   // compact boundary pairs + their reflection-2 partners (UP-Y outputs, DOWN inputs)
+            if (!in_int) { sa.iA = L.e2A; sa.iB = L.e2B; sa.is = L.e2s; }
+            if (!out_int) { sa.oA = L.e2A; sa.oB = L.e2B; sa.os = L.e2s; }
+            sa.sym2 = kind == 0 ? 0 : 1;
+            sa.xA2 = L.e2pA; sa.xB2 = L.e2pB; sa.xsA2 = L.e2sA; sa.xsB2 = L.e2sB;
+        }
         sa.n3 = L.n3; sa.next = L.next;
         const int bm = 8 * cfg.MT * cg_wm(cfg.WN);
         a.nrowblk = (a.rows + bm - 1) / bm;
@@ -1916,6 +1986,9 @@ int DeviceStore::plan_fused(const Tree& T) {
             a = FtArgs{};
             a.nlev = nlev; a.R2 = R2; a.hps = hstride; a.NE = NE;
             FtHostLevel hl[FT_MAXLEV];
+            bool any_sym2 = false;
+            for (int l = 0; l < nlev; ++l) any_sym2 = any_sym2 || levels[l0 + l].sym2;
+            if (any_sym2) { l0 += nlev; continue; }   // the fused kernels read the half-pair operator layout
             for (int l = 0; l < nlev; ++l) {
                 const Level& D = levels[l0 + l];
                 const MergeLevel& M = T.levels[l0 + l];
@@ -2049,6 +2122,11 @@ int DeviceStore::tune_stages(bool measure) {
         }
     }
     const char* env = std::getenv("REXP_AUTOTUNE");
+    if (measure && env && std::string(env) == "0" && !std::getenv("REXP_FUSE_FORCE")) {
+        // no measurements: the fused sweeps have not beaten the single-level launches anywhere yet
+        ft_up.clear();
+        ft_down.clear();
+    }
     if (!measure || (env && std::string(env) == "0")) return REXP_OK;
     // per-node store: only the GEMV shapes are candidates (no shared operator to
     // apply to many nodes at once)
@@ -2215,6 +2293,11 @@ std::string DeviceStore::stage_report() const {
         s += " L" + std::to_string(li + 1) + "[" + (levels[li].xdiag ? std::string("diag") : one(t_upx[li])) + "," +
              one(t_upy[li]) + "," + one(t_down[li]) + "]";
     s += shared ? std::string(" root[fourier]") : " root[" + one(t_root) + "]";
+    {
+        int n2 = 0;
+        for (const auto& L : levels) n2 += L.sym2 ? 1 : 0;
+        if (n2) s += " sym2[" + std::to_string(n2) + " levels]";
+    }
     for (const auto& g : ft_up) s += " fused_up[L" + std::to_string(g.l0 + 1) + "-L" + std::to_string(g.l0 + g.nlev) + "]";
     for (const auto& g : ft_down) s += " fused_down[L" + std::to_string(g.l0 + g.nlev) + "-L" + std::to_string(g.l0 + 1) + "]";
     if (!ft_times.empty()) s += " fused_vs_single:" + ft_times;

@@ -28,6 +28,15 @@ struct Level {
     double *sis = nullptr, *ses = nullptr;                                 // their signs
     std::vector<int> h_iA, h_iB, h_eA, h_eB;
     std::vector<double> h_is, h_es;
+    // second reflection (across the interface: it swaps the two children and leaves the
+    // interface fixed), R2 >= 16: only one boundary pair (A, B) of each reflection-2 orbit
+    // is computed (Y rows) / multiplied (S columns); e2* are compact over those hx2 pairs
+    bool sym2 = false;
+    int hx2 = 0;
+    int *e2A = nullptr, *e2B = nullptr, *e2pA = nullptr, *e2pB = nullptr;   // positions, partners (-1: none)
+    double *e2s = nullptr, *e2sA = nullptr, *e2sB = nullptr;                 // reflection-1 sign, partner signs
+    std::vector<int> h_e2A, h_e2B;
+    std::vector<double> h_e2s;
     double2 *X = nullptr, *Y = nullptr, *S = nullptr;   // [nh][nodes_stored][...] col-major
     int *ia3 = nullptr, *ib3 = nullptr, *ext = nullptr, *gext = nullptr, *g3 = nullptr;
     int *ia3p = nullptr, *ib3p = nullptr, *extc = nullptr, *extp = nullptr;   // node-independent forms (fused sweeps)
@@ -103,6 +112,7 @@ class DeviceStore {
     cudaEvent_t ev_fork = nullptr;
     void use_lane(int ln);
     int sym_pairs(const Tree& T, const MergeLevel& L, Level& D);
+    int sym_pairs2(const Tree& T, const MergeLevel& L, Level& D);
     std::vector<double> mode_parity;   // +-1: parity of eigenvector k of K under i -> q-1-i
     cudaGraphExec_t graph_exec = nullptr;
     const double* graph_state = nullptr;

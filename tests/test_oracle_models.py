@@ -175,3 +175,39 @@ def test_poles_counts_match_policy():
             pS, rS = compose_rational(prm["hS"], gaussian_coeffs_chi(prm["M0"]))
             err, mm = _check(*product_rational(pS, rS, pR, rR), A, 32)
             assert err > 1e-10 or mm > 1 + 1e-10
+
+
+def test_refined_lu_is_the_same_solve_with_a_smaller_residual():
+    """RefinedLU (reading R15) solves the SAME collocation system as a plain
+    sparse LU - the two solutions differ only at rounding level - and its
+    residual, evaluated independently in long double with dense arithmetic, is
+    smaller; on a tiny system it reproduces numpy's dense solve."""
+    import scipy.sparse.linalg as spla
+    from oracle.models import RefinedLU
+    m = Mesh(4, 12)
+    beta = (4.6 + 41.7j) / 0.2
+    B = m.collocation_matrix(np.full(m.NI, beta * beta + 1.0, dtype=complex))
+    rng = np.random.default_rng(3)
+    F = np.zeros(m.N, dtype=complex)
+    F[: m.NI] = rng.standard_normal(m.NI) + 1j * rng.standard_normal(m.NI)
+    x_plain = spla.splu(B.tocsc()).solve(F)
+    x_ref = RefinedLU(B).solve(F)
+    assert np.linalg.norm(x_ref - x_plain) <= 1e-10 * np.linalg.norm(x_plain)   # same system, same answer
+
+    def residual(x):   # independent of RefinedLU.residual: dense long-double products
+        Bd = B.toarray()
+        ld = np.longdouble
+        Br, Bi = Bd.real.astype(ld), Bd.imag.astype(ld)
+        xr, xi = x.real.astype(ld), x.imag.astype(ld)
+        rr = F.real.astype(ld) - (Br @ xr - Bi @ xi)
+        ri = F.imag.astype(ld) - (Br @ xi + Bi @ xr)
+        return float(np.sqrt((rr * rr + ri * ri).sum()))
+
+    r_plain, r_ref = residual(x_plain), residual(x_ref)
+    print(f"residual plain {r_plain:.2e} refined {r_ref:.2e}")
+    assert r_ref <= 0.5 * r_plain
+    # tiny system against the dense definition
+    m2 = Mesh(2, 6)
+    B2 = m2.collocation_matrix(np.full(m2.NI, 2.0 + 1.0j, dtype=complex))
+    F2 = rng.standard_normal(m2.N) + 1j * rng.standard_normal(m2.N)
+    assert np.linalg.norm(RefinedLU(B2).solve(F2) - np.linalg.solve(B2.toarray(), F2)) <= 1e-12 * np.linalg.norm(F2)

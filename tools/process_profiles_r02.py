@@ -124,7 +124,7 @@ def full_details(r):
     stall = [k for k in h if k.startswith("smsp__average_warps_issue_stalled_") and
              k.endswith("_per_issue_active.ratio")]
     dm = "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active"
-    lines = ["# ncu --set full --clock-control none -k regex:'k_cgemm|k_leaf_gemm|k_upx|k_root' --launch-count 40",
+    lines = ["# ncu --set full --clock-control none -k regex:'k_cgemm|k_leaf_gemm|k_upx|k_root|k_spec|k_recover' --launch-count 40",
              "#   python tools/profile_step.py --config c3_rsw_32x32_p16_x64   (one warm c3 step, first pole chunk)",
              "# columns: grid | time | DRAM GB, TB/s | warps active % | regs | DMMA-pipe % | FP64-pipe % | top stalls", ""]
     seen = set()

@@ -30,7 +30,7 @@ if [ "$STAGE" = all ] || [ "$STAGE" = ncu ]; then
         > $O/${R}_ncu_launch_${c%%_*}.log 2>&1
   done
   timeout 1500 ncu --profile-from-start off --set full --clock-control none --import-source on \
-      -k regex:'k_cgemm|k_leaf_gemm|k_upx|k_root' --launch-count 40 \
+      -k regex:'k_cgemm|k_leaf_gemm|k_upx|k_root|k_spec|k_recover' --launch-count 40 \
       -o /tmp/${R}_c3_full -f python tools/profile_step.py --config c3_rsw_32x32_p16_x64 > $O/${R}_ncu_full.log 2>&1
   ncu -i /tmp/${R}_c3_full.ncu-rep --page raw --csv > $O/${R}_c3_raw.csv 2>/dev/null
 fi
