@@ -191,6 +191,8 @@ def test_config0_fused_subtree_sweeps(c0, nrhs, up, down, monkeypatch):
     monkeypatch.setenv("REXP_FUSE_UP", up)
     monkeypatch.setenv("REXP_FUSE_DOWN", down)
     monkeypatch.setenv("REXP_FUSE_FORCE", "1")
+    if nrhs >= 8:   # the fused kernels read the half-pair operator layout (no second reflection)
+        monkeypatch.setenv("REXP_NO_SYM2", "1")
     U = np.stack([rsw_initial_state(m.x, m.y, cfg["seed"] + 10 * k) for k in range(nrhs)])
     h = _api().setup("rsw", cfg["n"], cfg["p"], cfg["tau"], cfg["delta"], Lam, f=cfg["f"], nrhs=nrhs)
     rep = h.stage_report
