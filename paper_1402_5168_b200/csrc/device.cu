@@ -1278,6 +1278,41 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
         if ((rc = put(&d_Aup, Aup))) return rc;
         if ((rc = put(&d_Adn, Adn))) return rc;
         store_bytes += static_cast<int64_t>(Aup.size() + Adn.size()) * 8;
+        {
+            // parity-split UP form (k_leaf_gemm_up_eo): e_1 = -Pi e_0, so side 1's coefficients are
+            // side 0's times the parity of the summed mode; rows (m, re|im), K = [even | odd modes]
+            std::vector<int> tE, tO;
+            for (int t = 0; t < q; ++t) (mode_parity[t] > 0 ? tE : tO).push_back(t);
+            double emax = 0.0, dev = 0.0;
+            for (int t = 0; t < q; ++t) {
+                emax = std::max(emax, std::fabs(E01[t]));
+                dev = std::max(dev, std::fabs(E01[SP_T + t] + mode_parity[t] * E01[t]));
+            }
+            lg_eo = dev <= 1e-11 * emax && nF * static_cast<int>(tE.size()) <= LG_KH &&
+                    nF * static_cast<int>(tO.size()) <= LG_KH && std::getenv("REXP_NO_LEAF_EO") == nullptr;
+            if (lg_eo) {
+                std::vector<int> kmap(LG_KP2, -1);
+                for (int f = 0; f < nF; ++f) {
+                    for (size_t i = 0; i < tE.size(); ++i) kmap[f * tE.size() + i] = f * q + tE[i];
+                    for (size_t i = 0; i < tO.size(); ++i) kmap[LG_KH + f * tO.size() + i] = f * q + tO[i];
+                }
+                const size_t MR2 = 2 * static_cast<size_t>(nh);
+                std::vector<double> A2(2 * q * MR2 * LG_KP2, 0.0);
+                for (int o = 0; o < 2; ++o)
+                    for (int r = 0; r < q; ++r) {
+                        const double* U = Aup.data() + (static_cast<size_t>(o) * q + r) * MR * KP;
+                        double* W = A2.data() + (static_cast<size_t>(o) * q + r) * MR2 * LG_KP2;
+                        for (int m = 0; m < nh; ++m)
+                            for (int c = 0; c < 2; ++c)
+                                for (int k = 0; k < LG_KP2; ++k)
+                                    if (kmap[k] >= 0)   // side 0's row of the (m, side, re|im) form
+                                        W[(2 * static_cast<size_t>(m) + c) * LG_KP2 + k] =
+                                            U[(4 * static_cast<size_t>(m) + c) * KP + kmap[k]];
+                    }
+                if ((rc = put(&d_Aup2, A2)) || (rc = put(&d_kmap, kmap))) return rc;
+                store_bytes += static_cast<int64_t>(A2.size()) * 8;
+            }
+        }
     }
     // operator store, filled by upload_ops (possibly in pole chunks)
     const size_t leaf_stored = shared ? 1 : static_cast<size_t>(nelem);
@@ -2333,7 +2368,16 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
         const dim3 gu(static_cast<unsigned>((4 * pc + ubm - 1) / ubm),
                       static_cast<unsigned>((lg.ncol + ubn - 1) / ubn), static_cast<unsigned>(2 * q));
         tbeg(s);
-        if (lg_KP == 44) lg_up_launch<44>(lg_up_var, gu, s, lg);
+        if (lg_eo) {
+            lg.Aup2 = d_Aup2 + static_cast<size_t>(2) * m0 * LG_KP2;
+            lg.aup2_os = static_cast<long long>(2) * nh * LG_KP2;
+            lg.kmap = d_kmap;
+            const int bn = lg_up_var == 1 ? 64 : 128;
+            const dim3 ge(static_cast<unsigned>((2 * pc + 31) / 32), static_cast<unsigned>((lg.ncol + bn - 1) / bn),
+                          static_cast<unsigned>(2 * q));
+            if (bn == 64) k_leaf_gemm_up_eo<32, 64, 2, 2><<<ge, 128, lg_up_eo_smem(32, 64), s>>>(lg);
+            else k_leaf_gemm_up_eo<32, 128, 2, 4><<<ge, 256, lg_up_eo_smem(32, 128), s>>>(lg);
+        } else if (lg_KP == 44) lg_up_launch<44>(lg_up_var, gu, s, lg);
         else lg_up_launch<48>(lg_up_var, gu, s, lg);
         tend(T_LEAF_UP, s);
     } else if (shared) {

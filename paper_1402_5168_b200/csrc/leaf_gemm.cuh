@@ -46,6 +46,10 @@ struct LeafGemmArgs {
     double2* h;               // [pc][hps][R2]
     long long hps;
     double c1;
+    // UP, parity-split form (k_leaf_gemm_up_eo): A rows 2 m + c, K = [even modes | odd modes]
+    const double* Aup2;       // [2q][2 nh][LG_KP2]
+    long long aup2_os;
+    const int* kmap;          // [LG_KP2] k -> f q + t (-1: padding)
     // DOWN
     const double* Adn;        // [2q][8 MT][lda] for this chunk: column 4 m0
     long long adn_os;         // doubles between (o, r) blocks
@@ -153,6 +157,110 @@ __global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm_up(LeafGemmArgs a) {
             dst[(size_t)leaf * 4 * q * a.R2 + r2] = ev ? make_double2(acc[i][n][0], y) : make_double2(y, acc[i][n][1]);
         }
     }
+}
+
+// --------------------------------------------------------------------------
+// UP, parity-split (round 2).  The eigenvectors of K are even or odd under the
+// node reversal, and the end rows of the differentiation matrix are mirror
+// images with opposite sign, so e_1 = -Pi e_0 (Pi = diag(mode parity)) and the
+// coefficients of the two sides of an orientation differ only by the parity of
+// the summed mode: A(side 1; t) = pi_t A(side 0; t).  With
+//   E = sum_{t even} A(side 0; f, t) G_f[t],   O = sum_{t odd} A(side 0; f, t) G_f[t]
+// the two sides are h_0 = E + O, h_1 = E - O: rows (m, re|im) only, K split into
+// [even | odd] halves of LG_KH columns accumulated separately - 0.55 of the
+// DMMAs of the (m, side, re|im) x (f, t) form.
+// --------------------------------------------------------------------------
+constexpr int LG_KH = 24, LG_KP2 = 2 * LG_KH;   // nF * ceil(q / 2) <= 24 for q <= 16
+
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(32 * WM * WN) k_leaf_gemm_up_eo(LeafGemmArgs a) {
+    constexpr int NT = 32 * WM * WN, KP = LG_KP2;
+    constexpr int TM = BM / WM, TN = BN / WN, MT = TM / 8, NTL = TN / 8;
+    constexpr int LDB = BN + 4;
+    static_assert(KP + 4 <= LG_LDK, "K padding");
+    extern __shared__ double lsm[];
+    double* As = lsm;                   // [BM][LG_LDK]
+    double* Bs = lsm + BM * LG_LDK;     // [KP][LDB]
+    const int q = a.q;
+    const int mt0 = blockIdx.x * BM, col0 = blockIdx.y * BN;
+    const int o = blockIdx.z / q, r = blockIdx.z % q;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int wm = wid / WN, wn = wid % WN;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int Mrows = a.Mrows / 2;      // 2 rows per half pole
+    const double* A = a.Aup2 + (size_t)blockIdx.z * a.aup2_os;
+    for (int e = tid; e < BM * (KP / 2); e += NT) {
+        const int row = e / (KP / 2), c2 = e % (KP / 2);
+        double* d = As + row * LG_LDK + 2 * c2;
+        if (mt0 + row < Mrows) cp_async16(d, A + (size_t)(mt0 + row) * KP + 2 * c2);
+        else { d[0] = 0.0; d[1] = 0.0; }
+    }
+    for (int e = tid; e < KP * (BN / 2); e += NT) {
+        const int kk = e / (BN / 2), c2 = e % (BN / 2);
+        double* d = Bs + kk * LDB + 2 * c2;
+        const int col = col0 + 2 * c2;
+        const int ft = a.kmap[kk];
+        if (ft >= 0 && col < a.ncol) {
+            const int f = ft / q, t = ft % q;
+            const int ip = o ? t : r, jp = o ? r : t;
+            cp_async16(d, a.G + ((size_t)(f * q + ip) * q + jp) * a.ncol + col);
+        } else {
+            d[0] = 0.0; d[1] = 0.0;
+        }
+    }
+    cp_async_commit();
+    double acc[2][MT][NTL][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int n = 0; n < NTL; ++n) acc[h][i][n][0] = acc[h][i][n][1] = 0.0;
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int ks = 0; ks < LG_KH / 4; ++ks) {
+            const int kk = h * LG_KH + ks * 4 + t4;
+            double av[MT], bv[NTL];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) av[i] = As[(wm * TM + i * 8 + g) * LG_LDK + kk];
+#pragma unroll
+            for (int n = 0; n < NTL; ++n) bv[n] = Bs[kk * LDB + wn * TN + n * 8 + g];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int n = 0; n < NTL; ++n) dmma884(acc[h][i][n][0], acc[h][i][n][1], av[i], bv[n]);
+        }
+    // epilogue: rows 2 m + c; threads g (even: re) and g + 1 (odd: im) of a quad column
+    // swap one value (lane ^ 4) and each stores one complex per side
+    const bool ev = (g & 1) == 0;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const int row = mt0 + wm * TM + i * 8 + g;
+        const int m = row >> 1;
+#pragma unroll
+        for (int n = 0; n < NTL; ++n) {
+            // side 0 = E + O, side 1 = E - O for this thread's two columns
+            const double s0a = acc[0][i][n][0] + acc[1][i][n][0], s0b = acc[0][i][n][1] + acc[1][i][n][1];
+            const double s1a = acc[0][i][n][0] - acc[1][i][n][0], s1b = acc[0][i][n][1] - acc[1][i][n][1];
+            const double y0 = __shfl_xor_sync(0xffffffffu, ev ? s0b : s0a, 4);
+            const double y1 = __shfl_xor_sync(0xffffffffu, ev ? s1b : s1a, 4);
+            if (2 * m >= Mrows) continue;
+            const int col = col0 + wn * TN + n * 8 + 2 * t4 + (ev ? 0 : 1);
+            if (col >= a.ncol) continue;
+            const int leaf = col / a.R2, r2 = col - leaf * a.R2;
+            const int sd0 = o ? 3 : 0, sd1 = o ? 1 : 2;
+            double2* d0 = a.h + ((size_t)m * a.hps + sd0 * q + r) * a.R2 + (size_t)leaf * 4 * q * a.R2 + r2;
+            double2* d1 = a.h + ((size_t)m * a.hps + sd1 * q + r) * a.R2 + (size_t)leaf * 4 * q * a.R2 + r2;
+            *d0 = ev ? make_double2(s0a, y0) : make_double2(y0, s0b);
+            *d1 = ev ? make_double2(s1a, y1) : make_double2(y1, s1b);
+        }
+    }
+}
+inline size_t lg_up_eo_smem(int BM, int BN) {
+    return ((size_t)BM * LG_LDK + (size_t)LG_KP2 * (BN + 4)) * sizeof(double);
 }
 
 // --------------------------------------------------------------------------
@@ -317,6 +425,7 @@ inline void lg_allow() {
     LG_ALLOW(k_leaf_gemm_up<44, 128, 64, 4, 2>); LG_ALLOW(k_leaf_gemm_up<44, 32, 128, 1, 4>);
     LG_ALLOW(k_leaf_gemm_up<48, 64, 128, 2, 4>); LG_ALLOW(k_leaf_gemm_up<48, 64, 64, 2, 2>);
     LG_ALLOW(k_leaf_gemm_up<48, 128, 64, 4, 2>); LG_ALLOW(k_leaf_gemm_up<48, 32, 128, 1, 4>);
+    LG_ALLOW(k_leaf_gemm_up_eo<32, 64, 2, 2>); LG_ALLOW(k_leaf_gemm_up_eo<32, 128, 2, 4>);
     LG_ALLOW(k_leaf_gemm_down<6, 128, 3>); LG_ALLOW(k_leaf_gemm_down<6, 128, 4>);
     LG_ALLOW(k_leaf_gemm_down<6, 64, 3>); LG_ALLOW(k_leaf_gemm_down<6, 64, 4>);
     LG_ALLOW(k_leaf_gemm_down<7, 128, 3>); LG_ALLOW(k_leaf_gemm_down<7, 128, 4>);

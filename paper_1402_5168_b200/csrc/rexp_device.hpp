@@ -125,6 +125,9 @@ class DeviceStore {
     double *d_G = nullptr, *d_Ehat = nullptr, *d_Eedge = nullptr, *d_Pi = nullptr;   // spectral RHS fields, pole-sum partials
     int* d_leaf_own = nullptr;                  // [nelem][4q] edge-node ownership for the pole sums
     double *d_Aup = nullptr, *d_Adn = nullptr;  // leaf GEMM coefficients (leaf_gemm.cuh), [2q][..]
+    double* d_Aup2 = nullptr;                   // parity-split UP coefficients (k_leaf_gemm_up_eo)
+    int* d_kmap = nullptr;
+    bool lg_eo = false;
     int lg_KP = 44, lg_MT = 6;                  // their K padding (UP) / row tiles (DOWN)
     int lg_up_var = 0, lg_dn_var = 0;           // tile variants (leaf_gemm.cuh)
     int ngroups = 1;                            // K slices of the leaf DOWN GEMM = pole-sum partial slots per lane
