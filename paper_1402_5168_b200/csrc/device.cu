@@ -17,6 +17,8 @@
 // to NB nodes, so each 16-byte load feeds NB*R2 complex FMAs.
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -1312,6 +1314,50 @@ int DeviceStore::init(const Problem& P, const Tree& T, const PoleTables& pt, int
                 if ((rc = put(&d_Aup2, A2)) || (rc = put(&d_kmap, kmap))) return rc;
                 store_bytes += static_cast<int64_t>(A2.size()) * 8;
             }
+            // parity-split DOWN form (k_leaf_gemm_down_eo): a1^ = Pi a0^; rows [even modes, edge-e |
+            // odd modes, edge-o], K = (m, re|im); needs equally many even and odd modes
+            double amax = 0.0, adev = 0.0;
+            for (int t = 0; t < q; ++t) {
+                amax = std::max(amax, std::fabs(A01[t]));
+                adev = std::max(adev, std::fabs(A01[SP_T + t] - mode_parity[t] * A01[t]));
+            }
+            const int nhm = static_cast<int>(tE.size());
+            lg_dn_mth = (nE * nhm + nE + 7) / 8;
+            const char* ev = std::getenv("REXP_LEAF_DOWN_EO");
+            lg_dn_eo = adev <= 1e-11 * amax && tE.size() == tO.size() && lg_dn_mth >= 2 && lg_dn_mth <= 4 &&
+                       lg_dn_var == 0 && !(ev && std::string(ev) == "0");
+            lg_dn_eo_pb = ev && std::string(ev) == "8" ? 8 : 4;
+            if (lg_dn_eo) {
+                const int rows = 16 * lg_dn_mth, G = 8 * lg_dn_mth;
+                std::vector<int> rmap(rows, INT_MIN);
+                const size_t L2 = 2 * static_cast<size_t>(nh);
+                std::vector<double> D2(2 * q * static_cast<size_t>(rows) * L2, 0.0);
+                for (int h = 0; h < 2; ++h) {
+                    const std::vector<int>& tt = h ? tO : tE;
+                    for (int k = 0; k < nE; ++k) {
+                        for (int i = 0; i < nhm; ++i) rmap[h * G + k * nhm + i] = k * q + tt[i];
+                        rmap[h * G + nE * nhm + k] = -1 - k;
+                    }
+                }
+                for (int o = 0; o < 2; ++o)
+                    for (int r = 0; r < q; ++r) {
+                        const double* Dd = Adn.data() + (static_cast<size_t>(o) * q + r) * MD * MR;
+                        double* W = D2.data() + (static_cast<size_t>(o) * q + r) * rows * L2;
+                        for (int row = 0; row < rows; ++row) {
+                            const int v = rmap[row];
+                            if (v == INT_MIN) continue;
+                            for (int m = 0; m < nh; ++m)
+                                for (int c = 0; c < 2; ++c) {
+                                    double x;
+                                    if (v >= 0) x = Dd[static_cast<size_t>(v) * MR + (2 * m + 0) * 2 + c];   // side 0's coefficient
+                                    else x = 0.5 * Dd[static_cast<size_t>(nE * q + 2 * (-1 - v) + 0) * MR + (2 * m + 0) * 2 + c];
+                                    W[static_cast<size_t>(row) * L2 + 2 * m + c] = x;
+                                }
+                        }
+                    }
+                if ((rc = put(&d_Adn2, D2)) || (rc = put(&d_rmap, rmap))) return rc;
+                store_bytes += static_cast<int64_t>(D2.size()) * 8;
+            }
         }
     }
     // operator store, filled by upload_ops (possibly in pole chunks)
@@ -2451,7 +2497,19 @@ int DeviceStore::tree_chunk(int m0, int pc, cudaStream_t s) {
         const int dbn = lg_dn_bn(lg_dn_var);
         const dim3 gd(static_cast<unsigned>((lg.ncol + dbn - 1) / dbn), static_cast<unsigned>(2 * q * ngroups));
         tbeg(s);
-        if (lg_MT == 6) lg_dn_launch<6>(lg_dn_var, gd, s, lg);
+        if (lg_dn_eo) {
+            lg.Adn2 = d_Adn2 + static_cast<size_t>(2) * m0;
+            lg.lda2 = 2 * nh;
+            lg.adn2_os = static_cast<long long>(16) * lg_dn_mth * lg.lda2;
+            lg.rmap = d_rmap;
+#define LG_DN_EO(MTH)                                                                                          \
+    if (lg_dn_eo_pb == 8) k_leaf_gemm_down_eo<MTH, 128, 2, 8><<<gd, 128, lg_dn_eo_smem<MTH, 128, 2, 8>(), s>>>(lg); \
+    else k_leaf_gemm_down_eo<MTH, 128, 3, 4><<<gd, 128, lg_dn_eo_smem<MTH, 128, 3, 4>(), s>>>(lg)
+            if (lg_dn_mth == 2) { LG_DN_EO(2); }
+            else if (lg_dn_mth == 3) { LG_DN_EO(3); }
+            else { LG_DN_EO(4); }
+#undef LG_DN_EO
+        } else if (lg_MT == 6) lg_dn_launch<6>(lg_dn_var, gd, s, lg);
         else lg_dn_launch<7>(lg_dn_var, gd, s, lg);
         tend(T_LEAF_DOWN, s);
     } else if (shared) {

@@ -50,6 +50,12 @@ struct LeafGemmArgs {
     const double* Aup2;       // [2q][2 nh][LG_KP2]
     long long aup2_os;
     const int* kmap;          // [LG_KP2] k -> f q + t (-1: padding)
+    // DOWN, parity-split form (k_leaf_gemm_down_eo): rows [even modes + edge-e | odd modes + edge-o],
+    // K = (m, re|im); operand u_0 + u_1 for the first row group, u_0 - u_1 for the second
+    const double* Adn2;       // [2q][16 MTH][lda2]
+    long long adn2_os;
+    int lda2;                 // 2 * nh
+    const int* rmap;          // [16 MTH] row -> k q + t (interior), -1 - k (edge sums), INT_MIN (padding)
     // DOWN
     const double* Adn;        // [2q][8 MT][lda] for this chunk: column 4 m0
     long long adn_os;         // doubles between (o, r) blocks
@@ -393,6 +399,149 @@ __global__ void __launch_bounds__(BN) k_leaf_gemm_down(LeafGemmArgs a) {
     }
 }
 
+// --------------------------------------------------------------------------
+// DOWN, parity-split (round 2).  a1^ = Pi a0^ (D2's end columns are mirror
+// images), so the coefficients of the two sides of an orientation differ by the
+// parity of the output mode t: A((k, t); m, side 1) = pi_t A((k, t); m, side 0).
+// Rows of even modes therefore contract with u_0 + u_1, rows of odd modes with
+// u_0 - u_1, both over K = (m, re|im) only: half the DMMAs.  The owned edge sums
+// sum_m Re(d_mk u_m[side]) ride along as a half-weight row in each group,
+// side 0 = e + o, side 1 = e - o (same thread: the groups have equal sizes).
+// Row groups of MTH m-tiles each; chunks of PB half poles (2 PB k).
+// --------------------------------------------------------------------------
+template <int MTH, int BN, int NST, int PB>
+constexpr size_t lg_dn_eo_smem() {
+    return (size_t)NST * ((size_t)16 * MTH * (2 * PB + 4) + (size_t)(2 * PB) * (2 * BN + 8)) * sizeof(double);
+}
+
+template <int MTH, int BN, int NST, int PB>
+__global__ void __launch_bounds__(BN) k_leaf_gemm_down_eo(LeafGemmArgs a) {
+    constexpr int MT = 2 * MTH, BM = 8 * MT, NT = BN, NTL = 4, LDP = 2 * BN + 8, BP = 2 * PB;
+    constexpr int BK = 2 * PB, LDA = BK + 4;
+    constexpr int ASZ = BM * LDA, BSZ = BP * LDP;
+    static_assert(BK % 4 == 0, "k-steps of 4");
+    extern __shared__ double lsm[];
+    const int q = a.q;
+    const int col0 = blockIdx.x * BN;
+    const int orr = blockIdx.y / a.ksplit, ks = blockIdx.y % a.ksplit;
+    const int o = orr / q, r = orr % q;
+    const int tid = threadIdx.x, lane = tid & 31, wn = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int npole = a.Kdn / 4;
+    const int pb = npole / a.ksplit, pr = npole % a.ksplit;
+    const int p0 = ks * pb + min(ks, pr), p1 = p0 + pb + (ks < pr ? 1 : 0);
+    const double* A = a.Adn2 + (size_t)orr * a.adn2_os;
+    const int bcol = col0 + tid;
+    const bool bok = bcol < a.ncol;
+    const int bleaf = bok ? bcol / a.R2 : 0, br2 = bok ? bcol - bleaf * a.R2 : 0;
+    const int sd0 = o ? 0 : 3, sd1 = o ? 2 : 1;
+    const long long ge0 = a.gB[(size_t)bleaf * 4 * q + sd0 * q + r];
+    const long long ge1 = a.gB[(size_t)bleaf * 4 * q + sd1 * q + r];
+    auto issue = [&](int st, int pp0) {
+        double* As = lsm + st * (ASZ + BSZ);
+        double* Bs = As + ASZ;
+        for (int e = tid; e < BM * (BK / 2); e += NT) {
+            const int row = e / (BK / 2), c2 = e % (BK / 2);
+            const int k = 2 * pp0 + 2 * c2;
+            double* d = As + row * LDA + 2 * c2;
+            if (k < 2 * p1) cp_async16(d, A + (size_t)row * a.lda2 + k);
+            else { d[0] = 0.0; d[1] = 0.0; }
+        }
+#pragma unroll
+        for (int pp = 0; pp < BP; ++pp) {
+            const int m = pp0 + (pp >> 1);
+            double* d = Bs + pp * LDP + 2 * tid;
+            if (bok && m < p1)
+                cp_async16(d, a.edge + ((size_t)m * a.NE + ((pp & 1) ? ge1 : ge0)) * a.R2 + br2);
+            else { d[0] = 0.0; d[1] = 0.0; }
+        }
+        cp_async_commit();
+    };
+    double acc[MT][NTL][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int n = 0; n < NTL; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
+    const int nch = (p1 - p0 + PB - 1) / PB;
+#pragma unroll
+    for (int st = 0; st < NST - 1; ++st) {
+        if (st < nch) issue(st, p0 + PB * st);
+        else cp_async_commit();
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        cp_async_wait_group<NST - 2>();
+        __syncthreads();
+        const int nx = ch + NST - 1;
+        if (nx < nch) issue(nx % NST, p0 + PB * nx);
+        else cp_async_commit();
+        const double* As = lsm + (ch % NST) * (ASZ + BSZ);
+        const double* Bs = As + ASZ;
+#pragma unroll
+        for (int kb = 0; kb < BK / 4; ++kb) {
+            const int kk = kb * 4 + t4;
+            double av[MT], be[NTL], bo[NTL];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) av[i] = As[(i * 8 + g) * LDA + kk];
+            // k = (pole 2 kb + (t4 >> 1), component t4 & 1): u_0 +- u_1 of that pole
+#pragma unroll
+            for (int n = 0; n < NTL; ++n) {
+                const int cidx = 2 * (wn * 32 + n * 8 + g) + (t4 & 1);
+                const double u0 = Bs[(2 * (2 * kb + (t4 >> 1))) * LDP + cidx];
+                const double u1 = Bs[(2 * (2 * kb + (t4 >> 1)) + 1) * LDP + cidx];
+                be[n] = u0 + u1;
+                bo[n] = u0 - u1;
+            }
+#pragma unroll
+            for (int i = 0; i < MTH; ++i)
+#pragma unroll
+                for (int n = 0; n < NTL; ++n) {
+                    dmma884(acc[i][n][0], acc[i][n][1], av[i], be[n]);
+                    dmma884(acc[MTH + i][n][0], acc[MTH + i][n][1], av[MTH + i], bo[n]);
+                }
+        }
+    }
+    double* Eh = a.Ehat + (size_t)(2 * ks + o) * a.ehat_ss;
+    double* Ee = a.Eedge + (size_t)ks * a.eedge_ss;
+#pragma unroll
+    for (int i = 0; i < MTH; ++i) {
+        const int row = i * 8 + g;
+        const int re = a.rmap[row], ro = a.rmap[8 * MTH + row];
+#pragma unroll
+        for (int n = 0; n < NTL; ++n)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int col = col0 + wn * 32 + n * 8 + 2 * t4 + j;
+                if (col >= a.ncol) continue;
+                const double ve = acc[i][n][j], vo = acc[MTH + i][n][j];
+                if (re >= 0) {   // interior modes (the two groups' rows are different modes)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int kt = h ? ro : re;
+                        if (kt < 0) continue;
+                        const int k = kt / q, t = kt % q;
+                        const int ip = o ? r : t, jp = o ? t : r;
+                        double* d = Eh + ((size_t)(k * q + ip) * q + jp) * a.ncol + col;
+                        double v = h ? vo : ve;
+                        if (a.accumulate) v += *d;
+                        *d = v;
+                    }
+                } else if (re > -1000000) {   // edge sums of k = -1 - re: side 0 = e + o, side 1 = e - o
+                    const int k = -1 - re;
+                    const int leaf = col / a.R2, r2 = col - leaf * a.R2;
+#pragma unroll
+                    for (int sdx = 0; sdx < 2; ++sdx) {
+                        const int b = (sdx ? sd1 : sd0) * q + r;
+                        if (!a.own[(size_t)leaf * 4 * q + b]) continue;
+                        double* d = Ee + ((size_t)k * a.NE + a.gB[(size_t)leaf * 4 * q + b]) * a.R2 + r2;
+                        double v = sdx ? ve - vo : ve + vo;
+                        if (a.accumulate) v += *d;
+                        *d = v;
+                    }
+                }
+            }
+    }
+}
+
 // variant ids (REXP_LGU / REXP_LGD): UP 0 = 64x128 (2x4 warps), 1 = 64x64 (2x2),
 // 2 = 128x64 (4x2), 3 = 32x128 (1x4); DOWN 0 = BN 128 / 3 stages, 1 = 128 / 4,
 // 2 = 64 / 3, 3 = 64 / 4
@@ -426,6 +575,9 @@ inline void lg_allow() {
     LG_ALLOW(k_leaf_gemm_up<48, 64, 128, 2, 4>); LG_ALLOW(k_leaf_gemm_up<48, 64, 64, 2, 2>);
     LG_ALLOW(k_leaf_gemm_up<48, 128, 64, 4, 2>); LG_ALLOW(k_leaf_gemm_up<48, 32, 128, 1, 4>);
     LG_ALLOW(k_leaf_gemm_up_eo<32, 64, 2, 2>); LG_ALLOW(k_leaf_gemm_up_eo<32, 128, 2, 4>);
+    LG_ALLOW(k_leaf_gemm_down_eo<2, 128, 3, 4>); LG_ALLOW(k_leaf_gemm_down_eo<3, 128, 3, 4>);
+    LG_ALLOW(k_leaf_gemm_down_eo<4, 128, 3, 4>); LG_ALLOW(k_leaf_gemm_down_eo<2, 128, 2, 8>);
+    LG_ALLOW(k_leaf_gemm_down_eo<3, 128, 2, 8>); LG_ALLOW(k_leaf_gemm_down_eo<4, 128, 2, 8>);
     LG_ALLOW(k_leaf_gemm_down<6, 128, 3>); LG_ALLOW(k_leaf_gemm_down<6, 128, 4>);
     LG_ALLOW(k_leaf_gemm_down<6, 64, 3>); LG_ALLOW(k_leaf_gemm_down<6, 64, 4>);
     LG_ALLOW(k_leaf_gemm_down<7, 128, 3>); LG_ALLOW(k_leaf_gemm_down<7, 128, 4>);

@@ -128,6 +128,10 @@ class DeviceStore {
     double* d_Aup2 = nullptr;                   // parity-split UP coefficients (k_leaf_gemm_up_eo)
     int* d_kmap = nullptr;
     bool lg_eo = false;
+    double* d_Adn2 = nullptr;                   // parity-split DOWN coefficients (k_leaf_gemm_down_eo)
+    int* d_rmap = nullptr;
+    bool lg_dn_eo = false;
+    int lg_dn_mth = 3, lg_dn_eo_pb = 4;
     int lg_KP = 44, lg_MT = 6;                  // their K padding (UP) / row tiles (DOWN)
     int lg_up_var = 0, lg_dn_var = 0;           // tile variants (leaf_gemm.cuh)
     int ngroups = 1;                            // K slices of the leaf DOWN GEMM = pole-sum partial slots per lane
