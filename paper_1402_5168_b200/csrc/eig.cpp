@@ -175,6 +175,35 @@ int real_eig(int q, const std::vector<double>& K, std::vector<double>& lam, std:
         lam[e] = num;
         for (int i = 0; i < q; ++i) V[i * q + e] = x[i];
     }
+    // K centro-symmetric (the interior block of a Chebyshev D2 is): its eigenvectors are even or
+    // odd under i -> q-1-i.  Inverse iteration returns them with a parity defect of ~1e-12; project
+    // each onto its parity so that V, and V^-1 computed from it below, are parity-symmetric to
+    // rounding - the parity-split leaf GEMMs (leaf_gemm.cuh) rely on e_1 = -Pi e_0, a1^ = Pi a0^
+    {
+        double asym = 0.0;
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j)
+                asym = std::max(asym, std::fabs(K[i * q + j] - K[(q - 1 - i) * q + (q - 1 - j)]));
+        if (asym <= 1e-12 * knorm) {
+            for (int e = 0; e < q; ++e) {
+                double dp = 0.0, dm = 0.0;
+                for (int i = 0; i < q; ++i) {
+                    dp += std::fabs(V[i * q + e] - V[(q - 1 - i) * q + e]);
+                    dm += std::fabs(V[i * q + e] + V[(q - 1 - i) * q + e]);
+                }
+                const double par = dp <= dm ? 1.0 : -1.0;
+                double nr = 0.0;
+                for (int i = 0; i < (q + 1) / 2; ++i) {
+                    const double v = 0.5 * (V[i * q + e] + par * V[(q - 1 - i) * q + e]);
+                    V[i * q + e] = v;
+                    V[(q - 1 - i) * q + e] = par * v;
+                }
+                for (int i = 0; i < q; ++i) nr += V[i * q + e] * V[i * q + e];
+                nr = std::sqrt(nr);
+                for (int i = 0; i < q; ++i) V[i * q + e] /= nr;
+            }
+        }
+    }
     // residual check ||K V - V L|| / ||K||
     double res = 0.0;
     for (int i = 0; i < q; ++i)
