@@ -185,13 +185,13 @@ PEAK_SOURCE = ("FP64: tools/fp64_peak.cu on this pool's B200 (profiles/r01_fp64_
 
 def class_bound(cls, shared, R2):
     """Which unit bounds a kernel class: the shared store's merge
-    stages are DMMA GEMMs (k_cgemm / k_cgemm_sym; a few-RHS run's top levels are
-    HBM-bound pair GEMVs), the spectral leaf kernels and the Fourier root run on
+    stages and leaf passes are DMMA GEMMs (k_cgemm / k_cgemm_sym / k_leaf_gemm_*; a
+    few-RHS run's top levels are HBM-bound pair GEMVs), the Fourier root runs on
     the FP64 FMA pipe; the per-node store streams its operators (HBM)."""
     if not shared:
         return "hbm"
-    if cls in ("merge_up", "merge_down"):
-        return "tensor"
+    if cls in ("merge_up", "merge_down", "leaf_up", "leaf_down"):
+        return "tensor"   # the leaf passes are DMMA GEMMs over the poles (leaf_gemm.cuh) since round 2
     return "alu"
 
 
