@@ -159,9 +159,18 @@ def class_work(cfg, nh, R2, shared, leaf="dense", nF=3, nE=3, sym2=False):
     }
     if leaf == "spectral":
         unit = nh * e * R2
+        # the parity-split leaf GEMMs (leaf_gemm.cuh, round 2) execute fewer flops than the spectral FMA
+        # form counted in round 1: UP 2q (o, r) x 2 rows x nF q x 2, DOWN 2q x (nE q + 2 nE) rows x 2 x 2
+        # per (half pole, leaf, real RHS); the count is the smaller of the two (no credit for padding)
+        up_fma, dn_fma = q2 * (4 * nF + 6 + 16), 16 * q2 + q2 * (8 + 4 * nE) + 8 * q * nE
+        eo_up = os.environ.get("REXP_NO_LEAF_EO") is None
+        mth = (nE * (q // 2) + nE + 7) // 8
+        eo_dn = eo_up and q % 2 == 0 and 2 <= mth <= 4 and os.environ.get("REXP_LEAF_DOWN_EO") != "0"
+        up_fl = min(up_fma, 8 * nF * q2) if eo_up else up_fma
+        dn_fl = min(dn_fma, 8 * q * (nE * q + 2 * nE)) if eo_dn else dn_fma
         w = {
-            "leaf_up": (unit * q2 * (4 * nF + 6 + 16), nh * q2 * 16),
-            "leaf_down": (unit * (16 * q2 + q2 * (8 + 4 * nE) + 8 * q * nE), nh * q2 * 16),
+            "leaf_up": (unit * up_fl, nh * q2 * 16),
+            "leaf_down": (unit * dn_fl, nh * q2 * 16),
         }
         w.update(merge)
         return w
